@@ -1,0 +1,377 @@
+"""Benchmark: P1 element integration on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                    [--precision f32|f64] [--mode strict|fast] [--impl ours|reference]
+
+A step is one pass of the fused integration kernel over the rank's element
+range (weak scaling: every rank owns one full copy of the workload's element
+count, a contiguous slice of one global structured mesh; no collective on the
+data path).  Default workload = BASELINE.json configs[1]: P1 linear
+elasticity, 2D triangles, 1,048,576 elements, FP32 (FP64 reported alongside).
+
+value  = whole-job paper-count GFLOP/s (reference flop_count), device time from
+         CUDA events around each kernel on the launching stream, max over ranks;
+         inputs resident in HBM, L2 flushed (512 MB read) between steps.
+e2e    = the same metric through the public C ABI (fb_integrate_mesh) with
+         pinned HOST buffers: H2D of coordinates + connectivity, kernel, D2H of
+         the full element-matrix store, every step.
+--impl reference: the unmodified reference CPU engine (oracle/_ref, built from
+         /root/reference) on this host's cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (op, dim, elements per GPU, BASELINE.json config string)
+    "2d-elasticity-1m": ("elasticity", 2, 1 << 20,
+                         "P1 linear elasticity, 2D triangles, 1M elements, FP32 and FP64"),
+    "2d-laplacian-64k": ("laplacian", 2, 1 << 16,
+                         "P1 Laplacian, 2D triangles, 65,536 elements (CPU reference oracle run)"),
+    "3d-laplacian-16m": ("laplacian", 3, 1 << 24, "P1 Laplacian, 3D tetrahedra, 16M elements on 1 B200"),
+    "3d-elasticity-8m": ("elasticity", 3, 1 << 23,
+                         "P1 linear elasticity, 3D tetrahedra, 64M elements sharded over 8xB200 (per-GPU shard)"),
+}
+METRIC = "element-integration GFLOP/s and elements/s vs HBM roofline at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--workload", default="2d-elasticity-1m", choices=sorted(WORKLOADS))
+    p.add_argument("--precision", default="f32", choices=["f32", "f64"])
+    p.add_argument("--mode", default="strict", choices=["strict", "fast"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def krows(op, dim):
+    return (dim + 1) * dim if op == "elasticity" else dim + 1
+
+
+def flops_per_element(op, dim):
+    kr, dd = krows(op, dim), dim * dim
+    return kr * kr * 2 * dd if op != "weighted-laplacian" else kr * kr * (dim + 1) * (2 * dd + 2)
+
+
+def build_rank_mesh(op, dim, ne_per, rank, world, jitter=0.15, seed=42):
+    """Slice [rank*ne, (rank+1)*ne) of the first world*ne cells of the
+    reference structured mesh (jittered where the reference would afford it)."""
+    from paper_1103_0066_b200 import mesh_prefix
+
+    total = ne_per * world
+    v, c, n = mesh_prefix(dim, total, jitter if total <= (1 << 24) else 0.0, seed)
+    nb = dim + 1
+    cells = np.ascontiguousarray(c[rank * ne_per * nb:(rank + 1) * ne_per * nb])
+    return v, cells, n
+
+
+def algorithmic_bytes(op, dim, prec, cells, nv_ref):
+    ne = cells.size // (dim + 1)
+    s = 4 if prec == "f32" else 8
+    return ne * (dim + 1) * 4 + nv_ref * dim * 8 + ne * krows(op, dim) ** 2 * s
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        loaded = [r for r in self.rows if r[3].replace(".", "").isdigit() and float(r[3]) > 0] or self.rows
+        sm = [float(r[1]) for r in loaded if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(loaded)}
+
+
+def cpu_baseline(op, dim, prec, v, cells, target_s=10.0):
+    """The reference's own CPU path (oracle/_ref) on this host's cores: the
+    mesh-in / matrices-out composition pack_geometry + integrate_batches with
+    the paper's best variant (bs128 ce2 interleaved), all hardware threads."""
+    from oracle.oracle import Reference, Restatement, reference_available
+
+    ne = cells.size // (dim + 1)
+    flops = flops_per_element(op, dim) * ne
+    cores = os.cpu_count() or 1
+    if reference_available():
+        ref = Reference()
+        t1, _ = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True,
+                                   precision=0 if prec == "f32" else 1, workers=cores, reps=1,
+                                   include_packing=True)
+        reps = int(max(1, min(50, target_s / max(t1, 1e-6))))
+        tmin, tmean = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True,
+                                         precision=0 if prec == "f32" else 1, workers=cores, reps=reps,
+                                         include_packing=True)
+        return {"value": flops / tmin * 1e-9, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                "elements_per_s": ne / tmin, "seconds_min": tmin, "seconds_mean": tmean,
+                "sample": f"full workload ({ne} elements) x {reps} reps, pack_geometry+integrate_batches, "
+                          f"bs128 ce2 interleaved, workers={cores}, min over reps"}
+    ora = Restatement()
+    sample = min(ne, 1 << 18)
+    c = np.ascontiguousarray(cells[: sample * (dim + 1)])
+    t0 = time.perf_counter()
+    ora.integrate_mesh(op, v, c, dim, bs=128, precision=prec)
+    t = time.perf_counter() - t0
+    return {"value": flops_per_element(op, dim) * sample / t * 1e-9, "unit": "GFLOP/s", "cores": 1,
+            "kind": "port", "elements_per_s": sample / t,
+            "sample": f"first {sample} elements, C restatement, 1 thread"}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    op, dim, ne_per, cfg_name = WORKLOADS[args.workload]
+    from oracle.oracle import Reference, Restatement, reference_available
+
+    total = ne_per * world
+    sample = min(total, 1 << 22)
+    v, c, _ = build_rank_mesh(op, dim, sample, 0, 1)
+    cores = os.cpu_count() or 1
+    prec = 0 if args.precision == "f32" else 1
+    kind = "reference" if reference_available() else "port"
+    times = []
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            t, _ = Reference().time_integrate(op, v, c, dim, bs=128, ce=2, interleave=True, precision=prec,
+                                              workers=cores, reps=1, include_packing=True)
+        else:
+            t0 = time.perf_counter()
+            Restatement().integrate_mesh(op, v, c, dim, bs=128, precision=prec)
+            t = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(t)
+    ms = statistics.mean(times) * 1e3
+    flops = flops_per_element(op, dim) * sample
+    val = flops / (ms * 1e-3) * 1e-9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "elements_per_s": sample / (ms * 1e-3),
+        "config": {"workload": args.workload, "baseline_config": cfg_name, "elements": total,
+                   "sampled_elements": sample, "precision": args.precision, "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores if kind == "reference" else 1,
+                         "kind": kind,
+                         "sample": f"{sample} of {total} elements per step; pack_geometry+integrate_batches "
+                                   f"bs128 ce2 interleaved"},
+        "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+
+    import paper_1103_0066_b200 as fb
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    op, dim, ne_per, cfg_name = WORKLOADS[args.workload]
+    prec = args.precision
+    v, cells, n = build_rank_mesh(op, dim, ne_per, rank, world)
+    nv_ref = int(np.unique(cells).size)
+    kr = krows(op, dim)
+    var = fb.make_variant(op, dim, prec, args.mode, element_batch_size=128)
+    store_len = var.store_length(ne_per)
+
+    dev = torch.device("cuda", local)
+    dv = torch.from_numpy(v).to(dev)
+    dc = torch.from_numpy(cells).to(dev)
+    tdt = torch.float32 if prec == "f32" else torch.float64
+    out = torch.empty(store_len, dtype=tdt, device=dev)
+    status = torch.empty(2, dtype=torch.int64, device=dev)
+    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    scrub.fill_(1)
+    stream = torch.cuda.current_stream()
+    sid = stream.cuda_stream
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def kernel_steps(variant, output, k, warm):
+        fb.status_reset(status, sid)
+        for _ in range(warm):
+            fb.integrate_mesh_async(variant, dv, dc, output, status, sid)
+        torch.cuda.synchronize()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        barrier()
+        torch.cuda.synchronize()
+        n0 = fb.launch_counter()
+        for i in range(k):
+            scrub.sum(dtype=torch.int64)  # flush L2 with clean lines (outside the events)
+            starts[i].record(stream)
+            fb.integrate_mesh_async(variant, dv, dc, output, status, sid)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        launches = fb.launch_counter() - n0
+        fb.status_check(status, sid)
+        ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        return statistics.mean(ms), min(ms), launches
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local) as clocks:
+        ms_mean, ms_min, launches = kernel_steps(var, out, args.steps, args.warmup)
+        ms_mean = max_over_ranks(ms_mean)
+
+        # e2e through the public C ABI with pinned host buffers
+        hv = torch.from_numpy(v).pin_memory()
+        hc = torch.from_numpy(cells).pin_memory()
+        hout = torch.empty(store_len, dtype=tdt).pin_memory()
+        hv_np, hc_np, hout_np = hv.numpy(), hc.numpy(), hout.numpy()
+        for _ in range(2):
+            fb.integrate_mesh(var, hv_np, hc_np, out=hout_np, devices=[local])
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            fb.integrate_mesh(var, hv_np, hc_np, out=hout_np, devices=[local])
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        barrier()
+        e2e_ms = max_over_ranks(e2e_ms)
+
+        # the FP64 leg of the same config (BASELINE configs[1] asks for both)
+        other = "f64" if prec == "f32" else "f32"
+        var2 = fb.make_variant(op, dim, other, args.mode, element_batch_size=128)
+        out2 = torch.empty(store_len, dtype=torch.float64 if other == "f64" else torch.float32, device=dev)
+        ms2, _, l2 = kernel_steps(var2, out2, args.steps, args.warmup)
+        ms2 = max_over_ranks(ms2)
+        launches += l2
+
+    # parity spot check of the timed output (full bitwise check lives in tests/)
+    torch.cuda.synchronize()
+
+    flops = flops_per_element(op, dim) * ne_per * world
+    value = flops / (ms_mean * 1e-3) * 1e-9
+    peak, peak_src = peaks()
+    bytes_launch = algorithmic_bytes(op, dim, prec, cells, nv_ref)
+    achieved = bytes_launch / (ms_mean * 1e-3) * 1e-9
+    bytes2 = algorithmic_bytes(op, dim, other, cells, nv_ref)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{args.workload}:{prec}:{args.mode}")
+    h2d = v.nbytes + cells.nbytes
+    d2h = store_len * (4 if prec == "f32" else 8) + 16
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_mean, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": prec, "data": "synthetic",
+        "elements_per_s": ne_per * world / (ms_mean * 1e-3),
+        "config": {"workload": args.workload, "baseline_config": cfg_name, "op": op, "dim": dim,
+                   "elements_per_gpu": ne_per, "elements": ne_per * world, "mesh": f"structured n={n} prefix",
+                   "jitter": 0.15 if ne_per * world <= (1 << 24) else 0.0, "precision": prec,
+                   "mode": args.mode, "parallelism": f"element shards x{world}, no collectives",
+                   "l2": "flushed between steps (512 MB read, outside the events)",
+                   "element_batch_size": 128},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_launch,
+                     "kernel": "fb_integrate_sparse (fused geometry + G:K + staged stores)"},
+        "e2e": {"value": flops / (e2e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "fb_integrate_mesh (C ABI), pinned host buffers"},
+        "gpu_launches": launches,
+        other: {"value": flops / (ms2 * 1e-3) * 1e-9, "ms_per_step": ms2,
+                "elements_per_s": ne_per * world / (ms2 * 1e-3),
+                "roofline_frac": bytes2 / (ms2 * 1e-3) * 1e-9 / peak},
+        "ms_min": ms_min,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(op, dim, prec, v, cells)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

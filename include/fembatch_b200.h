@@ -1,0 +1,203 @@
+/*
+ * fembatch_b200.h -- C-ABI drop-in boundary of the B200 P1 element-integration
+ * engine (libfembatch_b200.so).  Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj):
+ *
+ *   fb_specialize            <- fembatch::specialize_kernel      include/fembatch/engine.hpp:60-63,
+ *                                                                src/engine.cpp:301-337
+ *   fb_integrate_mesh        <- pack_geometry + integrate_batches (the composition every
+ *                               caller makes: src/bench.cpp:120-164, tests/test_engine.cpp:28-38)
+ *                               fused into one kernel: G never reaches HBM
+ *   fb_integrate_packed      <- fembatch::integrate_batches      include/fembatch/engine.hpp:65-70,
+ *                                                                src/engine.cpp:339-376
+ *   fb_pack_geometry         <- fembatch::pack_geometry          include/fembatch/geometry.hpp:91,
+ *                                                                src/geometry.cpp:312-351
+ *   fb_flop_count            <- fembatch::flop_count             src/engine.cpp:378-387
+ *   fb_element_matrix_index  <- fembatch::element_matrix_index   src/engine.cpp:287-299
+ *   fb_build_analytic_tensor <- fembatch::build_analytic_tensor  src/forms.cpp:234-246
+ *   fb_structured_mesh /     <- structured_simplicial_mesh /     src/geometry.cpp:164-262
+ *   fb_jitter_mesh              jitter_mesh (input synthesis)
+ *
+ * Errors: every call returns an fb_status code and, when `err` is non-NULL,
+ * fills it with the reference's exception text (same wording as the
+ * std::invalid_argument / std::runtime_error / std::out_of_range the
+ * reference throws) and, for degenerate cells, the lowest offending cell.
+ * All argument validation happens before any device work.
+ *
+ * Threading: every entry point is reentrant.  The library keeps one grow-only
+ * workspace and two streams per device, guarded by a per-device mutex, so
+ * concurrent calls that target the same device serialise; calls on different
+ * devices run concurrently.  No global mutable state is shared with callers.
+ */
+#ifndef FEMBATCH_B200_H
+#define FEMBATCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FB_ABI_VERSION 1
+
+/* Operators (reference Operator enum, include/fembatch/forms.hpp:12). */
+enum fb_operator { FB_LAPLACIAN = 0, FB_ELASTICITY = 1, FB_WEIGHTED_LAPLACIAN = 2 };
+
+/* Precision (reference Precision, include/fembatch/kernel_config.hpp:10). */
+enum fb_precision { FB_F32 = 0, FB_F64 = 1 };
+
+/* Arithmetic mode (GPU extension).
+ *   FB_STRICT: FP64 geometry with IEEE divisions in the reference's operation
+ *              order, no FMA contraction anywhere -> bitwise equal to the
+ *              reference engine (pack_geometry + integrate_batches).
+ *   FB_FAST:   FMA + one reciprocal of det; within the stated tolerances
+ *              (normwise 1e-13 f64, 5e-6 f32), not bitwise. */
+enum fb_mode { FB_STRICT = 0, FB_FAST = 1 };
+
+/* Output staging (GPU extension).  AUTO picks STAGED whenever the output
+ * pointer is 16-byte aligned. */
+enum fb_store { FB_STORE_AUTO = 0, FB_STORE_STAGED = 1, FB_STORE_DIRECT = 2 };
+
+enum fb_status {
+  FB_OK = 0,
+  FB_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  FB_ERR_RUNTIME = 2,          /* reference: std::runtime_error (degenerate cell) */
+  FB_ERR_OUT_OF_RANGE = 3,     /* reference: std::out_of_range */
+  FB_ERR_CUDA = 4,
+  FB_ERR_NO_DEVICE = 5
+};
+
+/* Reference KernelConfig (include/fembatch/kernel_config.hpp:23-37) plus the
+ * GPU extension fields.  The reference axes are value-neutral on the GPU
+ * exactly as on the CPU: element_batch_size fixes the padded store length
+ * (num_batches * bs * krows^2 scalars) and the bound/divisibility checks;
+ * num_concurrent_elements, interleave_stores and loop_unroll are validated
+ * and named in the variant description but never change a value. */
+typedef struct fb_kernel_config {
+  int32_t element_batch_size;      /* reference default 128 */
+  int32_t num_concurrent_elements; /* reference default 1 */
+  int32_t interleave_stores;       /* bool */
+  int32_t loop_unroll;             /* bool */
+  int32_t precision;               /* enum fb_precision */
+  int32_t mode;                    /* enum fb_mode (GPU) */
+  int32_t store;                   /* enum fb_store (GPU) */
+  int32_t reserved;                /* must be 0 */
+} fb_kernel_config;
+
+/* Reference Mesh (include/fembatch/geometry.hpp:14-35) as a borrowed view.
+ * vertices: num_vertices*dim doubles, vertex-major.
+ * cells:    num_elements*(dim+1) int32 vertex ids, element-major.
+ * Pointers may be host or device memory (detected per call). */
+typedef struct fb_mesh_view {
+  int32_t dim;
+  int32_t reserved;
+  int64_t num_vertices;
+  int64_t num_elements;
+  const double* vertices;
+  const int32_t* cells;
+} fb_mesh_view;
+
+typedef struct fb_error {
+  int32_t code;        /* enum fb_status */
+  int32_t reserved;
+  int64_t cell;        /* lowest offending cell for degenerate/out-of-range cells, else -1 */
+  char message[256];   /* reference exception text */
+} fb_error;
+
+/* A frozen kernel variant: spec + config + K cast to engine precision, with
+ * the K structure (P1 sparsity, symmetry, elasticity component blocks)
+ * validated once so the launch can pick the sparse kernel. */
+typedef struct fb_variant fb_variant;
+
+/* ---- library / devices -------------------------------------------------- */
+int fb_abi_version(void);
+int fb_device_count(void);
+/* Number of CUDA kernels this library has launched so far (all devices). */
+int64_t fb_launch_counter(void);
+
+/* ---- pure host helpers -------------------------------------------------- */
+int fb_krows(int op, int dim);
+int64_t fb_k_len(int op, int dim);
+int64_t fb_flop_count(int op, int dim, int64_t num_elements);
+int64_t fb_element_matrix_index(int krows, int element_batch_size,
+                                int num_concurrent_elements, int64_t element,
+                                int i, int j);
+/* num_batches * bs * krows^2 (the reference store length). */
+int64_t fb_store_length(int op, int dim, int64_t num_elements, int element_batch_size);
+int fb_build_analytic_tensor(int op, int dim, double* k_out, int64_t k_len,
+                             fb_error* err);
+
+/* ---- input synthesis (reference mesh generators) ------------------------ */
+int fb_structured_mesh_sizes(int dim, int n, int64_t* num_vertices,
+                             int64_t* num_elements);
+int fb_structured_mesh(int dim, int n, double* vertices, int32_t* cells,
+                       fb_error* err);
+/* In place: displace interior vertices (reference jitter_mesh semantics,
+ * bit-identical for a given seed); rejects tangled results. */
+int fb_jitter_mesh(int dim, double* vertices, int64_t num_vertices,
+                   const int32_t* cells, int64_t num_elements,
+                   double magnitude, uint64_t seed, fb_error* err);
+
+/* ---- variants ------------------------------------------------------------ */
+fb_variant* fb_specialize(int op, int dim, const double* k_blocks, int64_t k_len,
+                          const fb_kernel_config* config, fb_error* err);
+void fb_variant_free(fb_variant* v);
+/* "bs128_ce2_is_unroll"-style name (reference engine.cpp:329-335). */
+const char* fb_variant_description(const fb_variant* v);
+/* Kernel path chosen at specialize time: 0 = sparse+symmetric (P1 structure
+ * validated), 1 = sparse, 2 = dense fallback (arbitrary K). */
+int fb_variant_path(const fb_variant* v);
+
+/* ---- integration ---------------------------------------------------------
+ * out / out_len: the ElementMatrixStore scalars (engine precision), length
+ * exactly fb_store_length(); padding slots replicate the last element, as the
+ * reference computes them.  coefficients: num_elements*(dim+1) doubles for
+ * the weighted form (reference CoefficientField), else NULL.
+ *
+ * devices/ndev: host pointers are sharded over these devices by contiguous
+ * tile-aligned element ranges (no collectives; outputs concatenate).
+ * NULL/0 means device 0 (or, for device pointers, the pointers' device).
+ * Host buffers should be pinned for full PCIe bandwidth. */
+int fb_integrate_mesh(const fb_variant* v, const fb_mesh_view* mesh,
+                      const double* coefficients, void* out, int64_t out_len,
+                      const int* devices, int ndev, fb_error* err);
+
+/* G-input path: g = num_batches*bs*dim^2 scalars of engine precision in the
+ * reference PackedGeometry layout. */
+int fb_integrate_packed(const fb_variant* v, int dim, const void* g,
+                        int64_t num_batches, int64_t num_elements,
+                        const double* coefficients, void* out, int64_t out_len,
+                        const int* devices, int ndev, fb_error* err);
+
+/* GPU pack_geometry: g_out = num_batches*bs*dim^2 scalars (precision). */
+int fb_pack_geometry(const fb_mesh_view* mesh, int element_batch_size,
+                     int precision, void* g_out, int64_t g_len,
+                     const int* devices, int ndev, fb_error* err);
+
+/* ---- device-resident asynchronous API ------------------------------------
+ * All pointers are device pointers on the current device; the launch is
+ * enqueued on `stream` (a cudaStream_t, NULL = legacy default stream) and the
+ * call returns without synchronising.  `status` is a device buffer of two
+ * int64 words (lowest degenerate cell, lowest cell with an out-of-range
+ * vertex id): reset it with fb_status_reset, read it with fb_status_check. */
+int fb_integrate_mesh_async(const fb_variant* v, const fb_mesh_view* mesh,
+                            const double* coefficients, void* out,
+                            int64_t out_len, int64_t* status, void* stream,
+                            fb_error* err);
+int fb_integrate_packed_async(const fb_variant* v, int dim, const void* g,
+                              int64_t num_batches, int64_t num_elements,
+                              const double* coefficients, void* out,
+                              int64_t out_len, void* stream, fb_error* err);
+int fb_status_reset(int64_t* status, void* stream, fb_error* err);
+/* Synchronises `stream`, then maps the status words to the reference
+ * exception (FB_ERR_RUNTIME "degenerate element: det(J) <= 0 in cell N"). */
+int fb_status_check(const int64_t* status, void* stream, fb_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEMBATCH_B200_H */

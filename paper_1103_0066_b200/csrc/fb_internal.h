@@ -1,0 +1,75 @@
+// fb_internal.h -- interface between the C-ABI host layer (fb_capi.cpp) and
+// the sm_100a kernels (fb_kernels_*.cu).  Not installed; not part of the ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace fbk {
+
+// One CTA = 288 threads (9 warps).  288 = 2^5 * 9 is a multiple of every
+// output "period" (16-byte chunks per repeating group of element matrices):
+// 9, 4, 9, 36 chunks for f32 {2D-L, 3D-L, 2D-E, 3D-E} and 9, 8, 18, 72 for
+// f64, so in the store phase every thread owns a FIXED position inside an
+// element matrix and its source-row pattern is computed once per launch.
+constexpr int kThreads = 288;
+constexpr int kTile = 288;  // element slots per CTA tile (one per thread in phase 1)
+
+enum Op { kLaplacian = 0, kElasticity = 1, kWeighted = 2 };
+enum Mode { kStrict = 0, kFast = 1 };
+// kSparseSym: K validated to the P1 zero pattern, symmetric, and (elasticity)
+//             equal component-diagonal blocks -> nb(nb+1)/2 contractions.
+// kSparse:    P1 pattern, no symmetry shortcut (also used for packed G).
+// kDense:     arbitrary K, every dim^2 term, K read from device memory.
+enum Path { kSparseSym = 0, kSparse = 1, kDense = 2 };
+
+struct LaunchArgs {
+  const double* vtx = nullptr;     // full vertex array (device)
+  const int32_t* cells = nullptr;  // base-adjusted: cells + e*(dim+1) valid for touched e
+  const double* coeffs = nullptr;  // base-adjusted like cells (weighted form)
+  const void* g_in = nullptr;      // packed G, local slot-major (G-input path)
+  void* out = nullptr;             // local store (slot-major, krows^2 per slot)
+  const void* kdense = nullptr;    // dense path: K in engine precision (device)
+  long long* status = nullptr;     // [0] lowest degenerate cell, [1] lowest bad-index cell
+  int64_t nv = 0;                  // vertices
+  int64_t ne = 0;                  // real elements in the WHOLE mesh (padding clamp)
+  int64_t nloc = 0;                // slots handled by this launch
+  int64_t slot0 = 0;               // global slot index of local slot 0
+  int cells_aligned16 = 0;
+  int vtx_aligned16 = 0;
+};
+
+struct LaunchSpec {
+  int op = 0, dim = 2, prec = 1, mode = 0, path = 0;
+  int from_g = 0;   // 1 = G-input path
+  int staged = 1;   // 1 = smem-staged coalesced 16B stores, 0 = direct per-thread stores
+};
+
+// Sparse K values in engine precision, layout [((a*nb + b)*ncoef + c)*dim^2 + t]
+// for the (a, b) Laplacian-like block (component-0 block for elasticity).
+// Passed by value as a kernel parameter (constant bank, broadcast, reentrant).
+constexpr int kMaxKParamBytes = 16 * 4 * 9 * 8;  // 3D weighted f64 = 4608 B
+struct KParamBlob {
+  alignas(16) unsigned char bytes[kMaxKParamBytes];
+};
+
+// Per (precision, dim) translation units.
+cudaError_t launch_integrate_f32_2d(const LaunchSpec&, const LaunchArgs&, const KParamBlob&, cudaStream_t);
+cudaError_t launch_integrate_f32_3d(const LaunchSpec&, const LaunchArgs&, const KParamBlob&, cudaStream_t);
+cudaError_t launch_integrate_f64_2d(const LaunchSpec&, const LaunchArgs&, const KParamBlob&, cudaStream_t);
+cudaError_t launch_integrate_f64_3d(const LaunchSpec&, const LaunchArgs&, const KParamBlob&, cudaStream_t);
+cudaError_t launch_pack(int dim, int prec, const LaunchArgs&, cudaStream_t);
+
+inline cudaError_t launch_integrate(const LaunchSpec& s, const LaunchArgs& a,
+                                    const KParamBlob& k, cudaStream_t st)
+{
+  if (s.prec == 0)
+    return s.dim == 2 ? launch_integrate_f32_2d(s, a, k, st) : launch_integrate_f32_3d(s, a, k, st);
+  return s.dim == 2 ? launch_integrate_f64_2d(s, a, k, st) : launch_integrate_f64_3d(s, a, k, st);
+}
+
+inline int64_t num_tiles(int64_t nloc) { return (nloc + kTile - 1) / kTile; }
+
+}  // namespace fbk

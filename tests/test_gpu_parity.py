@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bar:
+* strict mode: BITWISE equal to the reference engine (pack_geometry +
+  integrate_batches) -- checked against the C restatement on seeded jittered
+  meshes and against golden fixtures produced by the unmodified reference;
+* fast mode: normwise per-element error vs the FP64 direct-quadrature oracle
+  <= 1e-13 (f64) and <= 5e-6 (f32);
+* connectivity / indexing / padding: exact.
+"""
+import numpy as np
+import pytest
+
+import paper_1103_0066_b200 as fb
+from oracle.oracle import OPS, krows, normwise_error
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-13, "f32": 5e-6}
+REF_TRI = np.array([[1.0, -0.5, -0.5], [-0.5, 0.5, 0.0], [-0.5, 0.0, 0.5]])
+
+
+def mesh(dim, n, jitter=0.15, seed=42):
+    return fb.structured_mesh(dim, n, jitter, seed)
+
+
+def coeffs_for(op, v, c, dim):
+    if op != "weighted-laplacian":
+        return None
+    # reference default_coefficient_field: w = 1 + x0 at each cell vertex (bench.cpp:19-30)
+    vv = v.reshape(-1, dim)
+    return np.ascontiguousarray((1.0 + vv[c.reshape(-1, dim + 1), 0]).ravel())
+
+
+@pytest.mark.parametrize("name", ["m2", "m3", "m2b"])
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("store", ["staged", "direct"])
+def test_strict_matches_reference_golden(golden, name, op, prec, store):
+    dim = 3 if name == "m3" else 2
+    bs = {"m2": 16, "m3": 7, "m2b": 128}[name]
+    v, c = golden[f"{name}_vertices"], golden[f"{name}_cells"]
+    w = golden[f"{name}_coeffs"] if op == "weighted-laplacian" else None
+    var = fb.make_variant(op, dim, prec, "strict", element_batch_size=bs, store=store)
+    got = fb.integrate_mesh(var, v, c, w)
+    p = 0 if prec == "f32" else 1
+    want = golden[f"{name}_store_{op}_p{p}"]
+    assert got.dtype == want.dtype and got.size == want.size
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("dim,n", [(2, 60), (3, 13)])
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_strict_bitwise_vs_restatement(restatement, dim, n, op, prec):
+    v, c = mesh(dim, n, 0.15, 42)
+    w = coeffs_for(op, v, c, dim)
+    for bs in (128, 100):
+        var = fb.make_variant(op, dim, prec, "strict", element_batch_size=bs)
+        assert var.path == 0  # P1 structure + symmetry validated -> sparse symmetric kernel
+        got = fb.integrate_mesh(var, v, c, w)
+        want = restatement.integrate_mesh(op, v, c, dim, bs=bs, precision=prec, coeffs=w)
+        assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("dim,n", [(2, 40), (3, 9)])
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_fast_within_tolerance_of_direct_oracle(restatement, dim, n, op, prec):
+    v, c = mesh(dim, n, 0.15, 42)
+    w = coeffs_for(op, v, c, dim)
+    var = fb.make_variant(op, dim, prec, "fast", element_batch_size=64)
+    got = fb.integrate_mesh(var, v, c, w)
+    ne = c.size // (dim + 1)
+    kr = krows(op, dim)
+    a = got[: ne * kr * kr].reshape(ne, kr, kr).transpose(0, 2, 1)  # store is j-major
+    want = restatement.direct_mesh(op, v, c, dim, w)
+    assert normwise_error(a, want) <= TOL[prec]
+    # strict is also within the same tolerance (sanity of the oracle metric)
+    s = fb.integrate_mesh(fb.make_variant(op, dim, prec, "strict", element_batch_size=64), v, c, w)
+    assert normwise_error(s[: ne * kr * kr].reshape(ne, kr, kr).transpose(0, 2, 1), want) <= TOL[prec]
+
+
+def test_reference_triangle_bitwise():
+    var = fb.make_variant("laplacian", 2, "f64", element_batch_size=1)
+    out = fb.integrate_mesh(var, np.array([0.0, 0, 1, 0, 0, 1]), np.array([0, 1, 2], dtype=np.int32))
+    assert np.array_equal(fb.unpack_element_matrix(out, 3, 0), REF_TRI)
+
+
+def test_synthetic_packed_geometry(golden):
+    # test_engine.cpp:337-378 through the G-input path, padded batch, exact
+    var = fb.make_variant("laplacian", 2, "f64", element_batch_size=4, num_concurrent_elements=2,
+                          interleave_stores=True, loop_unroll=True)
+    assert var.description == "bs4_ce2_is_unroll"
+    out = fb.integrate_batches(var, golden["synthetic_G"], 5)
+    assert out.size == 72
+    for e in range(5):
+        assert np.array_equal(fb.unpack_element_matrix(out, 3, e), (e + 1) * REF_TRI)
+    assert out.tobytes() == golden["synthetic_store"].tobytes()
+
+
+@pytest.mark.parametrize("dim,n", [(2, 30), (3, 7)])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_pack_and_packed_path_bitwise(restatement, dim, n, prec):
+    v, c = mesh(dim, n, 0.15, 3)
+    bs = 32
+    g = fb.pack_geometry(v, c, dim, bs, prec)
+    assert g.tobytes() == restatement.pack_geometry(v, c, dim, bs, prec).tobytes()
+    ne = c.size // (dim + 1)
+    for op in OPS:
+        w = coeffs_for(op, v, c, dim)
+        var = fb.make_variant(op, dim, prec, element_batch_size=bs)
+        got = fb.integrate_batches(var, g, ne, w)
+        want = restatement.integrate_packed(op, dim, g, ne, bs, prec, coeffs=w)
+        assert got.tobytes() == want.tobytes()
+        # fused == pack + integrate, bitwise
+        assert fb.integrate_mesh(var, v, c, w).tobytes() == got.tobytes()
+
+
+@pytest.mark.parametrize("op", list(OPS))
+def test_dense_fallback_for_unstructured_k(restatement, op):
+    dim = 2
+    v, c = mesh(dim, 12, 0.1, 5)
+    w = coeffs_for(op, v, c, dim)
+    k = fb.build_analytic_tensor(op, dim).copy()
+    kr, nc = krows(op, dim), (dim + 1 if op == "weighted-laplacian" else 1)
+    k[((1 + 1 * kr) * nc) * dim * dim + 1] = 0.125  # block (1,1), mu=0 nu=1: a structural zero
+    for prec in ("f32", "f64"):
+        var = fb.make_variant(op, dim, prec, k=k, element_batch_size=16)
+        assert var.path == 2
+        got = fb.integrate_mesh(var, v, c, w)
+        g = restatement.pack_geometry(v, c, dim, 16, prec)
+        want = restatement.integrate_packed(op, dim, g, c.size // 3, 16, prec, k=k, coeffs=w)
+        assert got.tobytes() == want.tobytes()
+
+
+def test_nonsymmetric_k_takes_sparse_path(restatement):
+    dim = 3
+    v, c = mesh(dim, 4, 0.1, 5)
+    k = fb.build_analytic_tensor("laplacian", dim).copy()
+    k[(0 + 1 * 4) * 9 + 3] *= 2.0  # block (0,1), mu=1 nu=0: still on the P1 pattern, asymmetric
+    var = fb.make_variant("laplacian", dim, "f64", k=k, element_batch_size=8)
+    assert var.path == 1
+    got = fb.integrate_mesh(var, v, c)
+    g = restatement.pack_geometry(v, c, dim, 8, 1)
+    want = restatement.integrate_packed("laplacian", dim, g, c.size // 4, 8, 1, k=k)
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("ne", [1, 2, 287, 288, 289, 1000, 4097])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_ragged_sizes_and_padding(restatement, ne, dim):
+    v, c, _ = fb.mesh_prefix(dim, ne, 0.1, 11)
+    for prec, op in (("f32", "laplacian"), ("f64", "elasticity")):
+        for bs in (1, 7, 128):
+            var = fb.make_variant(op, dim, prec, element_batch_size=bs)
+            got = fb.integrate_mesh(var, v, c)
+            want = restatement.integrate_mesh(op, v, c, dim, bs=bs, precision=prec)
+            assert got.tobytes() == want.tobytes()  # padding slots replicate the last element
+
+
+def test_empty_mesh():
+    var = fb.make_variant("laplacian", 3, "f32")
+    out = fb.integrate_mesh(var, np.zeros(12), np.zeros(0, dtype=np.int32))
+    assert out.size == 0
+    wv = fb.make_variant("weighted-laplacian", 2, "f64")
+    with pytest.raises(ValueError, match="zero elements"):
+        fb.integrate_mesh(wv, np.zeros(6), np.zeros(0, dtype=np.int32), np.zeros(3))
+
+
+def test_degenerate_cell_reports_lowest_index():
+    v, c = mesh(2, 8, 0.0)
+    c = c.copy()
+    c[5 * 3:5 * 3 + 3] = c[5 * 3:5 * 3 + 3][[0, 2, 1]]  # invert cell 5
+    c[40 * 3:40 * 3 + 3] = c[40 * 3:40 * 3 + 3][[0, 2, 1]]
+    for mode in ("strict", "fast"):
+        var = fb.make_variant("laplacian", 2, "f64", mode)
+        with pytest.raises(RuntimeError, match=r"degenerate element: det\(J\) <= 0 in cell 5") as ei:
+            fb.integrate_mesh(var, v, c)
+        assert ei.value.cell == 5
+
+
+def test_out_of_range_vertex_is_reported():
+    v, c = mesh(3, 2, 0.0)
+    c = c.copy()
+    c[9] = 10_000
+    var = fb.make_variant("laplacian", 3, "f64")
+    with pytest.raises(ValueError, match="out of range in cell 2"):
+        fb.integrate_mesh(var, v, c)
+
+
+def test_argument_validation_precedes_compute():
+    v, c = mesh(2, 3)
+    lap = fb.make_variant("laplacian", 2, "f64")
+    with pytest.raises(ValueError, match="form takes no coefficient field"):
+        fb.integrate_mesh(lap, v, c, np.ones(c.size))
+    wl = fb.make_variant("weighted-laplacian", 2, "f64")
+    with pytest.raises(ValueError, match="form requires a coefficient field"):
+        fb.integrate_mesh(wl, v, c)
+    l3 = fb.make_variant("laplacian", 3, "f64")
+    with pytest.raises(ValueError, match="geometry dimension does not match form"):
+        fb.integrate_mesh(l3, v, c[: 4 * 4])
+
+
+def test_device_tensors_and_async_api(restatement):
+    import torch
+
+    dim, op, prec = 3, "elasticity", "f32"
+    v, c = mesh(dim, 6, 0.15, 1)
+    var = fb.make_variant(op, dim, prec)
+    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+    out = fb.integrate_mesh(var, dv, dc)
+    assert out.is_cuda
+    want = restatement.integrate_mesh(op, v, c, dim, bs=128, precision=prec)
+    assert out.cpu().numpy().tobytes() == want.tobytes()
+    out2 = torch.empty_like(out)
+    status = torch.empty(2, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    fb.status_reset(status, s)
+    fb.integrate_mesh_async(var, dv, dc, out2, status, s)
+    fb.status_check(status, s)
+    assert torch.equal(out, out2)
+
+
+def test_multi_device_sharding_concatenates():
+    """devices=[0,0,0]: three contiguous tile-aligned shards on one GPU must
+    concatenate to the single-launch store bitwise."""
+    dim = 2
+    v, c, _ = fb.mesh_prefix(dim, 100_003, 0.1, 2)
+    for op, prec in (("elasticity", "f32"), ("laplacian", "f64")):
+        var = fb.make_variant(op, dim, prec, element_batch_size=64)
+        one = fb.integrate_mesh(var, v, c)
+        three = fb.integrate_mesh(var, v, c, devices=[0, 0, 0])
+        assert one.tobytes() == three.tobytes()
+
+
+def test_variant_invariance_bitwise():
+    # acceptance.cpp:175-215: every tuning axis is value-neutral
+    v, c = mesh(2, 10, 0.15, 42)
+    base = fb.integrate_mesh(fb.make_variant("laplacian", 2, "f32", element_batch_size=16), v, c)
+    ne = c.size // 3
+    for bs in (16, 32):
+        for ce in (1, 2, 4):
+            for is_ in (False, True):
+                for ur in (False, True):
+                    for store in ("staged", "direct"):
+                        var = fb.make_variant("laplacian", 2, "f32", element_batch_size=bs,
+                                              num_concurrent_elements=ce, interleave_stores=is_,
+                                              loop_unroll=ur, store=store)
+                        got = fb.integrate_mesh(var, v, c)
+                        assert got[: ne * 9].tobytes() == base[: ne * 9].tobytes()
+
+
+def test_launch_counter_counts_kernels():
+    v, c = mesh(2, 4)
+    var = fb.make_variant("laplacian", 2, "f64")
+    n0 = fb.launch_counter()
+    fb.integrate_mesh(var, v, c)
+    assert fb.launch_counter() - n0 == 1
