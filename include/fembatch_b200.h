@@ -148,7 +148,9 @@ void fb_variant_free(fb_variant* v);
 /* "bs128_ce2_is_unroll"-style name (reference engine.cpp:329-335). */
 const char* fb_variant_description(const fb_variant* v);
 /* Kernel path chosen at specialize time: 0 = sparse+symmetric (P1 structure
- * validated), 1 = sparse, 2 = dense fallback (arbitrary K). */
+ * validated), 1 = sparse, 2 = dense fallback (arbitrary K), 3 = sparse +
+ * symmetric + uniform magnitude (K = +-kappa on the P1 pattern, as the
+ * reference builds it). */
 int fb_variant_path(const fb_variant* v);
 
 /* ---- integration ---------------------------------------------------------

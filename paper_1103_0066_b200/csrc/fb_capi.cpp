@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -184,15 +185,40 @@ void analyse_k(fb_variant& v)
           if (ci == 0 && !(val == K(b, a, c, nu * dim + mu)))
             sym = false;
         }
-  v.path = !pattern ? fbk::kDense : (sym ? fbk::kSparseSym : fbk::kSparse);
+  // uniform magnitude: K = sigma_ab * kappa_c on the P1 pattern, sigma_ab = -1
+  // iff exactly one of a, b is 0 (reference gradients), kappa_c > 0 finite
+  bool uniform = pattern && sym;
+  std::vector<S> kappa(nc);
+  for (int c = 0; c < nc && uniform; ++c)
+  {
+    kappa[c] = K(0, 0, c, 0);
+    if (!(kappa[c] > S(0)) || !(kappa[c] < std::numeric_limits<S>::infinity()))
+      uniform = false;
+    for (int a = 0; a < nb && uniform; ++a)
+      for (int b = 0; b < nb && uniform; ++b)
+        for (int t = 0; t < dd; ++t)
+        {
+          const int mu = t / dim, nu = t % dim;
+          if (!((a == 0 || mu == a - 1) && (b == 0 || nu == b - 1)))
+            continue;
+          const S want = ((a == 0) != (b == 0)) ? -kappa[c] : kappa[c];
+          if (!(K(a, b, c, t) == want))
+            uniform = false;
+        }
+  }
+  v.path = !pattern ? fbk::kDense : (uniform ? fbk::kUniformSym : (sym ? fbk::kSparseSym : fbk::kSparse));
 
   static_assert(sizeof(fbk::KParamBlob) >= 16 * 4 * 9 * sizeof(double), "blob too small");
   S* kp = reinterpret_cast<S*>(v.kp.bytes);
-  for (int a = 0; a < nb; ++a)
-    for (int b = 0; b < nb; ++b)
-      for (int c = 0; c < nc; ++c)
-        for (int t = 0; t < dd; ++t)
-          kp[((a * nb + b) * nc + c) * dd + t] = K(a, b, c, t);
+  if (uniform)
+    for (int c = 0; c < nc; ++c)
+      kp[c] = kappa[c];
+  else
+    for (int a = 0; a < nb; ++a)
+      for (int b = 0; b < nb; ++b)
+        for (int c = 0; c < nc; ++c)
+          for (int t = 0; t < dd; ++t)
+            kp[((a * nb + b) * nc + c) * dd + t] = K(a, b, c, t);
 
   v.kdense.resize(v.k.size() * sizeof(S));
   S* kd = reinterpret_cast<S*>(v.kdense.data());

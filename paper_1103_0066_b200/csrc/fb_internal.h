@@ -23,7 +23,10 @@ enum Mode { kStrict = 0, kFast = 1 };
 //             equal component-diagonal blocks -> nb(nb+1)/2 contractions.
 // kSparse:    P1 pattern, no symmetry shortcut (also used for packed G).
 // kDense:     arbitrary K, every dim^2 term, K read from device memory.
-enum Path { kSparseSym = 0, kSparse = 1, kDense = 2 };
+// kUniformSym: kSparseSym and every nonzero entry is +-kappa_c with the P1
+//             gradient sign pattern (true of the reference's K): products
+//             g*kappa are shared between terms.
+enum Path { kSparseSym = 0, kSparse = 1, kDense = 2, kUniformSym = 3 };
 
 struct LaunchArgs {
   const double* vtx = nullptr;     // full vertex array (device)
@@ -70,6 +73,9 @@ inline cudaError_t launch_integrate(const LaunchSpec& s, const LaunchArgs& a,
   return s.dim == 2 ? launch_integrate_f64_2d(s, a, k, st) : launch_integrate_f64_3d(s, a, k, st);
 }
 
+#ifdef __CUDACC__
+__host__ __device__
+#endif
 inline int64_t num_tiles(int64_t nloc) { return (nloc + kTile - 1) / kTile; }
 
 }  // namespace fbk

@@ -11,21 +11,44 @@ namespace fbk {
 // Library-wide kernel launch counter (exported as fb_launch_counter()).
 std::atomic<long long>& launch_counter();
 
-template <class S, int DIM, int OP, int MODE, bool SYM, bool FROM_G, bool STAGED>
+// Persistent grid: every resident CTA slot on the device, capped by the tile
+// count (cached per kernel instantiation; all devices in a box are B200s).
+template <class F>
+unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std::atomic<int>& slots)
+{
+  int per = slots.load(std::memory_order_relaxed);
+  if (per == 0)
+  {
+    int blocks = 0, dev = 0, sms = 0;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    per = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
+    slots.store(per, std::memory_order_relaxed);
+  }
+  return (unsigned)(nctas < per ? nctas : per);
+}
+
+template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G, bool STAGED>
 cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st)
 {
   const KP<S, DIM, OP>& kp = *reinterpret_cast<const KP<S, DIM, OP>*>(kb.bytes);
-  fb_integrate_sparse<S, DIM, OP, MODE, SYM, FROM_G, STAGED>
-      <<<(unsigned)num_tiles(a.nloc), kThreads, 0, st>>>(a, kp);
+  auto kernel = fb_integrate_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, STAGED>;
+  constexpr size_t smem = sparse_smem_bytes<S, DIM, OP, SYM, STAGED>();
+  static std::atomic<int> slots{0};  // one cache per kernel instantiation
+  constexpr int threads = kWarpsPerCta * 32;
+  const int64_t nctas = (a.nloc + threads - 1) / threads;
+  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots), threads, smem, st>>>(a, kp);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
-template <class S, int DIM, int OP, int MODE, bool SYM, bool FROM_G>
+template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G>
 cudaError_t go_store(const LaunchSpec& s, const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st)
 {
-  return s.staged ? go_sparse<S, DIM, OP, MODE, SYM, FROM_G, true>(a, kb, st)
-                  : go_sparse<S, DIM, OP, MODE, SYM, FROM_G, false>(a, kb, st);
+  return s.staged ? go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, true>(a, kb, st)
+                  : go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, false>(a, kb, st);
 }
 
 template <class S, int DIM, int OP, int MODE>
@@ -34,9 +57,17 @@ cudaError_t go_mode(const LaunchSpec& s, const LaunchArgs& a, const KParamBlob& 
   // A caller-supplied G need not be symmetric, so the G-input path never
   // takes the symmetric shortcut.
   if (s.from_g)
-    return go_store<S, DIM, OP, MODE, false, true>(s, a, kb, st);
-  return s.path == kSparseSym ? go_store<S, DIM, OP, MODE, true, false>(s, a, kb, st)
-                              : go_store<S, DIM, OP, MODE, false, false>(s, a, kb, st);
+    return s.path == kUniformSym ? go_store<S, DIM, OP, MODE, false, true, true>(s, a, kb, st)
+                                 : go_store<S, DIM, OP, MODE, false, false, true>(s, a, kb, st);
+  switch (s.path)
+  {
+  case kUniformSym:
+    return go_store<S, DIM, OP, MODE, true, true, false>(s, a, kb, st);
+  case kSparseSym:
+    return go_store<S, DIM, OP, MODE, true, false, false>(s, a, kb, st);
+  default:
+    return go_store<S, DIM, OP, MODE, false, false, false>(s, a, kb, st);
+  }
 }
 
 template <class S, int DIM, int OP>

@@ -57,7 +57,7 @@ def test_strict_bitwise_vs_restatement(restatement, dim, n, op, prec):
     w = coeffs_for(op, v, c, dim)
     for bs in (128, 100):
         var = fb.make_variant(op, dim, prec, "strict", element_batch_size=bs)
-        assert var.path == 0  # P1 structure + symmetry validated -> sparse symmetric kernel
+        assert var.path == 3  # P1 structure, symmetry, uniform magnitude validated
         got = fb.integrate_mesh(var, v, c, w)
         want = restatement.integrate_mesh(op, v, c, dim, bs=bs, precision=prec, coeffs=w)
         assert got.tobytes() == want.tobytes()
@@ -134,6 +134,26 @@ def test_dense_fallback_for_unstructured_k(restatement, op):
         assert got.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("op", list(OPS))
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_symmetric_nonuniform_k_takes_sparse_sym_path(restatement, op, prec):
+    dim = 3
+    v, c = mesh(dim, 4, 0.1, 5)
+    w = coeffs_for(op, v, c, dim)
+    k = fb.build_analytic_tensor(op, dim).copy()
+    kr, nc, dd = krows(op, dim), (dim + 1 if op == "weighted-laplacian" else 1), dim * dim
+    for comp in range(dim if op == "elasticity" else 1):  # scale block (a=1,b=1) on every component
+        i = 1 + comp * (dim + 1)
+        k[(i + i * kr) * nc * dd:(i + i * kr + 1) * nc * dd] *= 3.0
+    var = fb.make_variant(op, dim, prec, k=k, element_batch_size=8)
+    assert var.path == 0
+    got = fb.integrate_mesh(var, v, c, w)
+    g = restatement.pack_geometry(v, c, dim, 8, prec)
+    want = restatement.integrate_packed(op, dim, g, c.size // 4, 8, prec, k=k, coeffs=w)
+    assert got.tobytes() == want.tobytes()
+    assert fb.integrate_batches(var, g, c.size // 4, w).tobytes() == want.tobytes()
+
+
 def test_nonsymmetric_k_takes_sparse_path(restatement):
     dim = 3
     v, c = mesh(dim, 4, 0.1, 5)
@@ -197,9 +217,18 @@ def test_argument_validation_precedes_compute():
     wl = fb.make_variant("weighted-laplacian", 2, "f64")
     with pytest.raises(ValueError, match="form requires a coefficient field"):
         fb.integrate_mesh(wl, v, c)
+    import ctypes as C
+
+    from paper_1103_0066_b200 import _lib
+
     l3 = fb.make_variant("laplacian", 3, "f64")
-    with pytest.raises(ValueError, match="geometry dimension does not match form"):
-        fb.integrate_mesh(l3, v, c[: 4 * 4])
+    mv = fb.engine.mesh_view(v, c, 2)  # a 2D mesh handed to a 3D variant
+    out = np.zeros(l3.store_length(c.size // 3))
+    err = _lib.fb_error()
+    rc = _lib.load().fb_integrate_mesh(l3.handle, C.byref(mv), None, out.ctypes.data, out.size, None, 0,
+                                       C.byref(err))
+    assert rc == _lib.FB_ERR_INVALID_ARGUMENT
+    assert err.message.decode() == "geometry dimension does not match form"
 
 
 def test_device_tensors_and_async_api(restatement):
