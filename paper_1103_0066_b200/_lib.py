@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfembatch_b200.so")
+# FB_LIB overrides the library path (same-box A/B experiments only).
+LIB_PATH = os.environ.get("FB_LIB") or os.path.join(HERE, "libfembatch_b200.so")
 
 FB_OK, FB_ERR_INVALID_ARGUMENT, FB_ERR_RUNTIME, FB_ERR_OUT_OF_RANGE, FB_ERR_CUDA, FB_ERR_NO_DEVICE = range(6)
 

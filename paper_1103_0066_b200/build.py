@@ -49,34 +49,40 @@ def _run(cmd, verbose):
     return r.stdout + r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Build the library.  `defines` (e.g. ["FB_PIPE=1"]) and `out` exist for
+    same-box A/B experiments (tools/kbench.py with FB_LIB=<path>)."""
     srcs = [os.path.join(CSRC, s) for s in CU_SOURCES + CPP_SOURCES + HEADERS] + PUBLIC_HEADERS
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest(srcs + [__file__]):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= _newest(srcs + [__file__]):
+        return out
+    build_dir = BUILD if out == LIB else BUILD + "_" + os.path.basename(out).replace(".so", "")
+    os.makedirs(build_dir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     inc = ["-I", CSRC, "-I", os.path.join(ROOT, "include")]
     jobs = []
     for s in CU_SOURCES:
-        obj = os.path.join(BUILD, s + ".o")
+        obj = os.path.join(build_dir, s + ".o")
         jobs.append((obj, [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
-                           "-Xptxas", "-v", *inc, "-c", os.path.join(CSRC, s), "-o", obj]))
+                           "-Xptxas", "-v", *dflags, *inc, "-c", os.path.join(CSRC, s), "-o", obj]))
     for s in CPP_SOURCES:
-        obj = os.path.join(BUILD, s + ".o")
+        obj = os.path.join(build_dir, s + ".o")
         jobs.append((obj, ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-pthread",
                            "-I", os.path.join(CUDA_HOME, "include"), *inc,
                            "-c", os.path.join(CSRC, s), "-o", obj]))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
-        for out in ex.map(lambda j: _run(j[1], verbose), jobs):
-            logs.append(out)
-    with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        logs.extend(ex.map(lambda j: _run(j[1], verbose), jobs))
+    with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[j[0] for j in jobs],
           "-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"], verbose)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, defines=defs,
+                out=outs[0] if outs else LIB))

@@ -368,12 +368,30 @@ void element_window(const Job& j, int64_t s0, int64_t s1, int64_t& lo, int64_t& 
   hi = std::min(std::max(s1, lo + 1), j.ne);
 }
 
+// Kernels index slots with 32-bit locals: split launches at 2^30 slots.
+constexpr int64_t kMaxLaunchSlots = int64_t(1) << 30;
+
+void launch_integrate_chunked(const fbk::LaunchSpec& spec, const fbk::LaunchArgs& a, const fbk::KParamBlob& kp,
+                              int nk, int dd, size_t ss, cudaStream_t st)
+{
+  for (int64_t off = 0; off < a.nloc; off += kMaxLaunchSlots)
+  {
+    fbk::LaunchArgs c = a;
+    c.slot0 = a.slot0 + off;
+    c.nloc = std::min(kMaxLaunchSlots, a.nloc - off);
+    c.out = static_cast<char*>(a.out) + off * nk * ss;
+    if (a.g_in)
+      c.g_in = static_cast<const char*>(a.g_in) + off * dd * ss;
+    cuda_check(fbk::launch_integrate(spec, c, kp, st), "integrate kernel launch");
+  }
+}
+
 void launch(const Job& j, const fbk::LaunchArgs& a, cudaStream_t st)
 {
   if (j.kind == Kind::Pack)
     cuda_check(fbk::launch_pack(j.dim, j.prec, a, st), "pack kernel launch");
   else
-    cuda_check(fbk::launch_integrate(j.spec, a, j.var->kp, st), "integrate kernel launch");
+    launch_integrate_chunked(j.spec, a, j.var->kp, j.nk, j.dim * j.dim, scalar_size(j.prec), st);
 }
 
 // Runs slots [s0, s1) of the job on device `dev`.  Host buffers are staged in
@@ -921,8 +939,8 @@ int fb_integrate_mesh_async(const fb_variant* vp, const fb_mesh_view* mesh, cons
                    fbk::LaunchSpec s = spec_of(v, false);
                    if (!aligned16(out))
                      s.staged = 0;
-                   cuda_check(fbk::launch_integrate(s, a, v.kp, static_cast<cudaStream_t>(stream)),
-                              "integrate kernel launch");
+                   launch_integrate_chunked(s, a, v.kp, v.krows * v.krows, v.dim * v.dim,
+                                            scalar_size(v.cfg.precision), static_cast<cudaStream_t>(stream));
                  });
 }
 
@@ -952,8 +970,8 @@ int fb_integrate_packed_async(const fb_variant* vp, int dim, const void* g, int6
                    fbk::LaunchSpec s = spec_of(v, true);
                    if (!aligned16(out))
                      s.staged = 0;
-                   cuda_check(fbk::launch_integrate(s, a, v.kp, static_cast<cudaStream_t>(stream)),
-                              "integrate kernel launch");
+                   launch_integrate_chunked(s, a, v.kp, v.krows * v.krows, v.dim * v.dim,
+                                            scalar_size(v.cfg.precision), static_cast<cudaStream_t>(stream));
                  });
 }
 

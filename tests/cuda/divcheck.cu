@@ -31,9 +31,10 @@ __device__ double draw(uint64_t r, int regime, int which)
   case 1:  // any finite exponent
     e = 1 + (r >> 52) % 2046;
     break;
-  case 2:  // guard boundaries: a tiny/huge, b moderate
-    e = which == 0 ? ((r >> 52) & 1 ? 90 + (r >> 53) % 80 : 1900 + (r >> 53) % 147)
-                   : 900 + (r >> 52) % 250;
+  case 2:  // guard boundaries: a and b around the 2^+-500 / 2^+-400 windows and CUDA's own limits
+    e = which == 0 ? ((r >> 52) & 1 ? ((r >> 53) & 1 ? 90 + (r >> 54) % 80 : 503 + (r >> 54) % 40)
+                                    : ((r >> 53) & 1 ? 1900 + (r >> 54) % 147 : 1503 + (r >> 54) % 40))
+                   : ((r >> 52) & 1 ? 603 + (r >> 53) % 40 : 1403 + (r >> 53) % 40);
     break;
   default:  // specials: zeros, denormals, inf, nan mixed with normals
   {
