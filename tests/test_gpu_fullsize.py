@@ -1,0 +1,94 @@
+"""Parity at the BASELINE.json configuration sizes.
+
+* 2D P1 elasticity, 1,048,576 elements (configs[1]), f32 and f64, strict:
+  the whole store bitwise against the oracle restatement.
+* 2D P1 Laplacian, 65,536 elements (configs[0]): bitwise + normwise vs the
+  FP64 direct-quadrature oracle on every element, fast mode within tolerance.
+* 3D P1 Laplacian, 16,777,216 elements (configs[2]) and one 8,388,608-element
+  shard of 3D elasticity-64M (configs[3]): sampled elements bitwise against the
+  oracle (every 4096th plus the first and last 4096), and size-independent
+  properties over the full store on the device: symmetry, zero row sums
+  (constants in the null space), elasticity's zero off-diagonal component
+  blocks and 0.25-scaled Laplacian diagonal blocks, bitwise.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_1103_0066_b200 as fb
+from oracle.oracle import krows, normwise_error
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _sample(ne):
+    idx = np.concatenate([np.arange(min(4096, ne)), np.arange(0, ne, 4096), np.arange(max(0, ne - 4096), ne)])
+    return np.unique(idx)
+
+
+def _device_mesh(dim, ne, jitter):
+    v, c, _ = fb.mesh_prefix(dim, ne, jitter, 42)
+    return v, c, torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_2d_elasticity_1m_bitwise(restatement, prec):
+    v, c, dv, dc = _device_mesh(2, 1 << 20, 0.15)
+    var = fb.make_variant("elasticity", 2, prec)
+    got = fb.integrate_mesh(var, dv, dc).cpu().numpy()
+    want = restatement.integrate_mesh("elasticity", v, c, 2, bs=128, precision=prec)
+    assert got.tobytes() == want.tobytes()
+
+
+def test_2d_laplacian_64k_against_direct_oracle(restatement):
+    v, c, dv, dc = _device_mesh(2, 1 << 16, 0.15)
+    ne = c.size // 3
+    direct = restatement.direct_mesh("laplacian", v, c, 2)
+    for prec, tol in (("f64", 1e-13), ("f32", 5e-6)):
+        for mode in ("strict", "fast"):
+            got = fb.integrate_mesh(fb.make_variant("laplacian", 2, prec, mode), dv, dc).cpu().numpy()
+            a = got[: ne * 9].reshape(ne, 3, 3).transpose(0, 2, 1)
+            assert normwise_error(a, direct) <= tol
+            if mode == "strict":
+                want = restatement.integrate_mesh("laplacian", v, c, 2, bs=128, precision=prec)
+                assert got.tobytes() == want.tobytes()
+
+
+def _properties(store, op, dim, ne):
+    kr = krows(op, dim)
+    nb = dim + 1
+    m = store[: ne * kr * kr].view(ne, kr, kr).transpose(1, 2)  # [e][i][j]
+    assert torch.equal(m, m.transpose(1, 2)), "not bitwise symmetric"
+    if op == "elasticity":
+        blocks = m.view(ne, dim, nb, dim, nb)  # [e][c][a][d][b]
+        lap = blocks[:, 0, :, 0, :]
+        for c in range(dim):
+            for d in range(dim):
+                blk = blocks[:, c, :, d, :]
+                if c == d:
+                    assert torch.equal(blk, lap)
+                else:
+                    assert torch.count_nonzero(blk).item() == 0
+        m = lap
+    scale = m.abs().amax(dim=(1, 2))
+    rows = m.double().sum(dim=2).abs().amax(dim=1)
+    tol = 1e-5 if store.dtype == torch.float32 else 1e-13
+    assert (rows <= tol * scale.double()).all().item(), "row sums are not ~0"
+
+
+@pytest.mark.parametrize("op,dim,ne,jitter,prec", [
+    ("laplacian", 3, 1 << 24, 0.15, "f32"),
+    ("elasticity", 3, 1 << 23, 0.0, "f32"),
+])
+def test_large_3d_sampled_bitwise_and_properties(restatement, op, dim, ne, jitter, prec):
+    v, c, dv, dc = _device_mesh(dim, ne, jitter)
+    var = fb.make_variant(op, dim, prec)
+    store = fb.integrate_mesh(var, dv, dc)
+    torch.cuda.synchronize()
+    _properties(store, op, dim, ne)
+    kr2 = krows(op, dim) ** 2
+    idx = _sample(ne)
+    cs = np.ascontiguousarray(c.reshape(-1, dim + 1)[idx].ravel())
+    want = restatement.integrate_mesh(op, v, cs, dim, bs=1, precision=prec).reshape(-1, kr2)
+    got = store.view(-1, kr2)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert got.tobytes() == want.tobytes()
