@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -103,52 +102,65 @@ def algorithmic_bytes(op, dim, prec, cells, nv_ref):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock and throttle reasons sampled through NVML (nvidia-ml-py) every
+    ~2 ms; mark()/unmark() bracket the timed regions so the summary reflects
+    the clocks the measured kernels actually ran at."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.rows = []
-        self.proc = None
+        self.samples = []  # (in_timed_region, sm_mhz, reasons_mask)
+        self.timed = False
+        self.stop = threading.Event()
+        self.max_mhz = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((self.timed, mhz, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
+    def mark(self):
+        self.timed = True
+
+    def unmark(self):
+        self.timed = False
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        loaded = [r for r in self.rows if r[3].replace(".", "").isdigit() and float(r[3]) > 0] or self.rows
-        sm = [float(r[1]) for r in loaded if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(loaded)}
+        timed = [s for s in self.samples if s[0]] or self.samples
+        if not timed:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mask = 0
+        for s in timed:
+            mask |= s[2]
+        return {"sm_mhz": statistics.median(s[1] for s in timed), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(k for k, bit in self.REASONS.items() if mask & bit),
+                "samples": len(timed), "source": "nvml 2 ms polling inside the timed regions"}
 
 
 def cpu_baseline(op, dim, prec, v, cells, target_s=10.0):
@@ -277,12 +289,14 @@ def main():
         barrier()
         torch.cuda.synchronize()
         n0 = fb.launch_counter()
+        clocks.mark()
         for i in range(k):
             scrub.sum(dtype=torch.int64)  # flush L2 with clean lines (outside the events)
             starts[i].record(stream)
             fb.integrate_mesh_async(variant, dv, dc, output, status, sid)
             ends[i].record(stream)
         torch.cuda.synchronize()
+        clocks.unmark()
         barrier()
         launches = fb.launch_counter() - n0
         fb.status_check(status, sid)
@@ -308,10 +322,12 @@ def main():
         for _ in range(2):
             fb.integrate_mesh(var, hv_np, hc_np, out=hout_np, devices=[local])
         barrier()
+        clocks.mark()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             fb.integrate_mesh(var, hv_np, hc_np, out=hout_np, devices=[local])
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        clocks.unmark()
         barrier()
         e2e_ms = max_over_ranks(e2e_ms)
 
