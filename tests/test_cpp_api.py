@@ -7,12 +7,13 @@ import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BIN = os.path.join(HERE, "cpp", "_bin", "test_api")
+CBIN = os.path.join(HERE, "cpp", "_bin", "test_c_abi")
 
 
-def _binary():
-    if not os.path.exists(BIN):
+def _binary(path=BIN):
+    if not os.path.exists(path):
         subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
-    return BIN
+    return path
 
 
 def test_cpp_api_host_cases():
@@ -26,3 +27,14 @@ def test_cpp_api_gpu_cases():
     r = subprocess.run([_binary(), "all"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_c_abi_from_plain_c_host():
+    r = subprocess.run([_binary(CBIN), "cpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_c_abi_from_plain_c_gpu():
+    r = subprocess.run([_binary(CBIN), "all"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
