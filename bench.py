@@ -249,12 +249,20 @@ def main():
 
     import paper_1103_0066_b200 as fb
 
+    ndev = torch.cuda.device_count()
+    local = local % max(ndev, 1)  # >1 rank per GPU only when testing the N>1 path on a 1-GPU box
     torch.cuda.set_device(local)
     dist = None
+    backend = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU over NCCL; gloo only if ranks outnumber GPUs (test mode)
+        backend = "nccl" if ndev >= world else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     op, dim, ne_per, cfg_name = WORKLOADS[args.workload]
     prec = args.precision
@@ -306,7 +314,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -365,6 +373,7 @@ def main():
                    "elements_per_gpu": ne_per, "elements": ne_per * world, "mesh": f"structured n={n} prefix",
                    "jitter": 0.15 if ne_per * world <= (1 << 24) else 0.0, "precision": prec,
                    "mode": args.mode, "parallelism": f"element shards x{world}, no collectives",
+                   "dist_backend": backend,
                    "l2": "flushed between steps (512 MB read, outside the events)",
                    "element_batch_size": 128},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

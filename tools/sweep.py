@@ -1,0 +1,124 @@
+"""Element-count sweep (BASELINE.json configs[4]): N = 2^12 ... 2^28 elements
+for {Laplacian, elasticity} x {2D, 3D} x {f32, f64}, strict mode, on G GPUs of
+this process (contiguous tile-aligned element shards, one per device, no
+collectives; time = max over devices of CUDA-event kernel time, inputs
+resident, L2 flushed between steps).  Writes CSV rows to stdout and to
+profiles/<out>.csv.
+
+    python tools/sweep.py [--gpus G] [--min-log2 12] [--max-log2 28] [--step 2] [--out r01_sweep_1gpu]
+
+Meshes are prefixes of the reference structured mesh (unjittered: jitter
+changes values, not bytes or flops).  Points whose per-GPU store exceeds
+--max-store-gb are skipped (3D elasticity f64 at 2^28 needs 309 GB).
+"""
+import argparse
+import csv
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1103_0066_b200 as fb  # noqa: E402
+from paper_1103_0066_b200.shard import shard_bounds  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--min-log2", type=int, default=12)
+    p.add_argument("--max-log2", type=int, default=28)
+    p.add_argument("--step", type=int, default=2)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--max-store-gb", type=float, default=120.0)
+    p.add_argument("--ops", default="laplacian,elasticity")
+    p.add_argument("--dims", default="2,3")
+    p.add_argument("--precisions", default="f32,f64")
+    p.add_argument("--out", default="r01_sweep_1gpu")
+    a = p.parse_args()
+    peak, _ = bench.peaks()
+    G = min(a.gpus, torch.cuda.device_count())
+    scrubs = [torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{d}") for d in range(G)]
+    for s in scrubs:
+        s.fill_(1)
+    fields = ["op", "dim", "precision", "elements", "gpus", "ms", "gbytes_per_s", "roofline_fraction",
+              "gflops", "gelem_per_s", "status"]
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    path = os.path.join(ROOT, "profiles", a.out + ".csv")
+    f = open(path, "w", newline="")
+    w = csv.DictWriter(f, fieldnames=fields)
+    w.writeheader()
+    sizes = [1 << k for k in range(a.min_log2, a.max_log2 + 1, a.step)]
+    for dim in [int(x) for x in a.dims.split(",")]:
+        v, c, _ = fb.mesh_prefix(dim, sizes[-1], 0.0, 42)
+        nb = dim + 1
+        for N in sizes:
+            cN = c[: N * nb]
+            nv_ref = int(np.unique(cN).size) if N <= (1 << 24) else int(cN.max()) + 1
+            for op in a.ops.split(","):
+                for prec in a.precisions.split(","):
+                    kr = bench.krows(op, dim)
+                    s = 4 if prec == "f32" else 8
+                    row = {"op": op, "dim": dim, "precision": prec, "elements": N, "gpus": G}
+                    if N * kr * kr * s / G > a.max_store_gb * 1e9:
+                        row["status"] = "skipped: store exceeds per-GPU budget"
+                        w.writerow(row)
+                        f.flush()
+                        print(row, flush=True)
+                        continue
+                    var = fb.make_variant(op, dim, prec)
+                    b = shard_bounds(N, G)
+                    shards = []
+                    for d in range(G):
+                        with torch.cuda.device(d):
+                            cs = torch.from_numpy(np.ascontiguousarray(cN[b[d] * nb:b[d + 1] * nb])).cuda(d)
+                            vs = torch.from_numpy(v).cuda(d)
+                            out = torch.empty(var.store_length(b[d + 1] - b[d]), device=f"cuda:{d}",
+                                              dtype=torch.float32 if prec == "f32" else torch.float64)
+                            st = torch.empty(2, dtype=torch.int64, device=f"cuda:{d}")
+                            shards.append((vs, cs, out, st))
+                    times = []
+                    for it in range(2 + a.steps):
+                        evs = []
+                        for d in range(G):
+                            with torch.cuda.device(d):
+                                sid = torch.cuda.current_stream().cuda_stream
+                                scrubs[d].sum(dtype=torch.int64)
+                                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                                vs, cs, out, st = shards[d]
+                                if it == 0:
+                                    fb.status_reset(st, sid)
+                                e0.record()
+                                if cs.numel():
+                                    fb.integrate_mesh_async(var, vs, cs, out, st, sid)
+                                e1.record()
+                                evs.append((e0, e1))
+                        for d in range(G):
+                            torch.cuda.synchronize(d)
+                        if it >= 2:
+                            times.append(max(e0.elapsed_time(e1) for e0, e1 in evs))
+                    for d in range(G):
+                        with torch.cuda.device(d):
+                            fb.status_check(shards[d][3], torch.cuda.current_stream().cuda_stream)
+                    del shards
+                    ms = statistics.median(times)
+                    by = N * nb * 4 + nv_ref * dim * 8 + N * kr * kr * s
+                    gbs = by / (ms * 1e-3) * 1e-9
+                    row.update(ms=round(ms, 5), gbytes_per_s=round(gbs, 1),
+                               roofline_fraction=round(gbs / (peak * G), 4),
+                               gflops=round(bench.flops_per_element(op, dim) * N / (ms * 1e-3) * 1e-9, 1),
+                               gelem_per_s=round(N / (ms * 1e-3) * 1e-9, 3), status="ok")
+                    w.writerow(row)
+                    f.flush()
+                    print(row, flush=True)
+    f.close()
+    print("wrote", path)
+
+
+if __name__ == "__main__":
+    main()
