@@ -57,9 +57,14 @@ enum fb_precision { FB_F32 = 0, FB_F64 = 1 };
  *              (normwise 1e-13 f64, 5e-6 f32), not bitwise. */
 enum fb_mode { FB_STRICT = 0, FB_FAST = 1 };
 
-/* Output staging (GPU extension).  AUTO picks STAGED whenever the output
- * pointer is 16-byte aligned. */
-enum fb_store { FB_STORE_AUTO = 0, FB_STORE_STAGED = 1, FB_STORE_DIRECT = 2 };
+/* Output path (GPU extension).  Element matrices are staged per warp tile in
+ * shared memory and leave it by TMA store (TMA: bulk or tensor store, where
+ * the staged layout allows it) or by a warp block copy LDS.128 -> STG.128
+ * (STAGED); DIRECT stores each lane's matrix from registers.  AUTO picks
+ * per layout the faster of TMA and STAGED as measured on B200.
+ * All give identical values; a store pointer that is not 16-byte aligned
+ * falls back to DIRECT. */
+enum fb_store { FB_STORE_AUTO = 0, FB_STORE_STAGED = 1, FB_STORE_DIRECT = 2, FB_STORE_TMA = 3 };
 
 enum fb_status {
   FB_OK = 0,

@@ -31,6 +31,7 @@ CU_SOURCES = [
     "fb_pack.cu",
 ]
 CPP_SOURCES = ["fb_capi.cpp", "fb_host.cpp", "fembatch_api.cpp"]
+CU_HOST_SOURCES = ["fb_tma.cpp"]  # host code that includes the kernel headers (nvcc)
 HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "fembatch_b200.h"),
                   os.path.join(ROOT, "include", "fembatch_b200.hpp")]
@@ -52,7 +53,7 @@ def _run(cmd, verbose):
 def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
     """Build the library.  `defines` (e.g. ["FB_PIPE=1"]) and `out` exist for
     same-box A/B experiments (tools/kbench.py with FB_LIB=<path>)."""
-    srcs = [os.path.join(CSRC, s) for s in CU_SOURCES + CPP_SOURCES + HEADERS] + PUBLIC_HEADERS
+    srcs = [os.path.join(CSRC, s) for s in CU_SOURCES + CU_HOST_SOURCES + CPP_SOURCES + HEADERS] + PUBLIC_HEADERS
     if not force and os.path.exists(out) and os.path.getmtime(out) >= _newest(srcs + [__file__]):
         return out
     build_dir = BUILD if out == LIB else BUILD + "_" + os.path.basename(out).replace(".so", "")
@@ -64,6 +65,10 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB
         obj = os.path.join(build_dir, s + ".o")
         jobs.append((obj, [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
                            "-Xptxas", "-v", *dflags, *inc, "-c", os.path.join(CSRC, s), "-o", obj]))
+    for s in CU_HOST_SOURCES:
+        obj = os.path.join(build_dir, s + ".o")
+        jobs.append((obj, [NVCC, *ARCH, "-O3", "-std=c++17", "-x", "cu", "-Xcompiler", "-fPIC",
+                           *dflags, *inc, "-c", os.path.join(CSRC, s), "-o", obj]))
     for s in CPP_SOURCES:
         obj = os.path.join(build_dir, s + ".o")
         jobs.append((obj, ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-pthread",

@@ -140,7 +140,7 @@ void validate_config(const fb_kernel_config& c)
     invalid("unknown precision");
   if (c.mode != FB_STRICT && c.mode != FB_FAST)
     invalid("unknown arithmetic mode");
-  if (c.store < FB_STORE_AUTO || c.store > FB_STORE_DIRECT)
+  if (c.store < FB_STORE_AUTO || c.store > FB_STORE_TMA)
     invalid("unknown store strategy");
 }
 
@@ -644,7 +644,7 @@ fbk::LaunchSpec spec_of(const fb_variant& v, bool from_g)
   s.mode = v.cfg.mode;
   s.path = v.path;
   s.from_g = from_g ? 1 : 0;
-  s.staged = v.cfg.store == FB_STORE_DIRECT ? 0 : 1;
+  s.staged = v.cfg.store == FB_STORE_DIRECT ? 0 : v.cfg.store == FB_STORE_STAGED ? 1 : v.cfg.store == FB_STORE_TMA ? 2 : 3;
   return s;
 }
 

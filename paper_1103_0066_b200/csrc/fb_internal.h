@@ -9,13 +9,10 @@
 
 namespace fbk {
 
-// One CTA = 288 threads (9 warps).  288 = 2^5 * 9 is a multiple of every
-// output "period" (16-byte chunks per repeating group of element matrices):
-// 9, 4, 9, 36 chunks for f32 {2D-L, 3D-L, 2D-E, 3D-E} and 9, 8, 18, 72 for
-// f64, so in the store phase every thread owns a FIXED position inside an
-// element matrix and its source-row pattern is computed once per launch.
+// CTA shape of the dense fallback and pack_geometry kernels (one slot per
+// thread); the sparse kernel uses persistent 128-thread CTAs (fb_kernels.cuh).
 constexpr int kThreads = 288;
-constexpr int kTile = 288;  // element slots per CTA tile (one per thread in phase 1)
+constexpr int kTile = 288;  // element slots per CTA tile
 
 enum Op { kLaplacian = 0, kElasticity = 1, kWeighted = 2 };
 enum Mode { kStrict = 0, kFast = 1 };
@@ -47,7 +44,9 @@ struct LaunchArgs {
 struct LaunchSpec {
   int op = 0, dim = 2, prec = 1, mode = 0, path = 0;
   int from_g = 0;   // 1 = G-input path
-  int staged = 1;   // 1 = smem-staged coalesced 16B stores, 0 = direct per-thread stores
+  int staged = 3;   // 0 = direct per-lane stores, 1 = smem staging + LDS/STG block copy,
+                    // 2 = smem staging + TMA store where the layout allows (else 1),
+                    // 3 = auto (per layout: the faster of 1 and 2, measured)
 };
 
 // Sparse K values in engine precision, layout [((a*nb + b)*ncoef + c)*dim^2 + t]

@@ -30,16 +30,30 @@ unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std:
   return (unsigned)(nctas < per ? nctas : per);
 }
 
-template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G, bool STAGED>
+// Tensor map of a launch's store viewed as rows of one element matrix
+// (krows^2 scalars) for the TMA store of swizzled warp tiles: box = 32 rows,
+// swizzle = the row size (64 / 128 bytes).  False if the driver entry point is
+// unavailable or the encoding is rejected (the caller then uses the LDS/STG
+// copy).
+bool encode_store_map(CUtensorMap* tm, void* out, int64_t rows, int row_scalars, int scalar_bytes);
+
+template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G, int ST>
 cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st)
 {
+  using WS = WarpStore<S, DIM, OP, SYM>;
   const KP<S, DIM, OP>& kp = *reinterpret_cast<const KP<S, DIM, OP>*>(kb.bytes);
-  auto kernel = fb_integrate_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, STAGED>;
-  constexpr size_t smem = sparse_smem_bytes<S, DIM, OP, SYM, STAGED>();
+  CUtensorMap tm{};
+  if constexpr (ST == kStTma && WS::TMA == 2)
+  {
+    if (!encode_store_map(&tm, a.out, a.nloc, WS::NK, (int)sizeof(S)))
+      return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStCopy>(a, kb, st);
+  }
+  auto kernel = fb_integrate_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, ST>;
+  constexpr size_t smem = sparse_smem_bytes<S, DIM, OP, SYM, ST>();
   static std::atomic<int> slots{0};  // one cache per kernel instantiation
   constexpr int threads = kWarpsPerCta * 32;
   const int64_t nctas = (a.nloc + threads - 1) / threads;
-  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots), threads, smem, st>>>(a, kp);
+  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots), threads, smem, st>>>(a, kp, tm);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -47,8 +61,26 @@ cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st
 template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G>
 cudaError_t go_store(const LaunchSpec& s, const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st)
 {
-  return s.staged ? go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, true>(a, kb, st)
-                  : go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, false>(a, kb, st);
+  switch (s.staged)
+  {
+  case kStDirect:
+    return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStDirect>(a, kb, st);
+  case kStCopy:
+    return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStCopy>(a, kb, st);
+  case kStTma:
+    // TMA wherever the staged layout has a TMA form (else identical to copy)
+    if constexpr (WarpStore<S, DIM, OP, SYM>::TMA != 0)
+      return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStTma>(a, kb, st);
+    else
+      return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStCopy>(a, kb, st);
+  default:
+    // auto: the 1D bulk store of linear layouts measured faster than the
+    // LDS/STG copy; the swizzled tensor store measured slower
+    if constexpr (WarpStore<S, DIM, OP, SYM>::TMA == 1)
+      return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStTma>(a, kb, st);
+    else
+      return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStCopy>(a, kb, st);
+  }
 }
 
 template <class S, int DIM, int OP, int MODE>

@@ -21,7 +21,7 @@ from . import _lib as L
 OPERATORS = {"laplacian": 0, "elasticity": 1, "weighted-laplacian": 2}
 PRECISIONS = {"f32": 0, "f64": 1}
 MODES = {"strict": 0, "fast": 1}
-STORES = {"auto": 0, "staged": 1, "direct": 2}
+STORES = {"auto": 0, "staged": 1, "direct": 2, "tma": 3}
 WORK_GROUP_BOUND = 1024
 
 

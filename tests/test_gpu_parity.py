@@ -35,7 +35,7 @@ def coeffs_for(op, v, c, dim):
 @pytest.mark.parametrize("name", ["m2", "m3", "m2b"])
 @pytest.mark.parametrize("op", list(OPS))
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-@pytest.mark.parametrize("store", ["staged", "direct"])
+@pytest.mark.parametrize("store", ["auto", "staged", "tma", "direct"])
 def test_strict_matches_reference_golden(golden, name, op, prec, store):
     dim = 3 if name == "m3" else 2
     bs = {"m2": 16, "m3": 7, "m2b": 128}[name]
@@ -272,7 +272,7 @@ def test_variant_invariance_bitwise():
         for ce in (1, 2, 4):
             for is_ in (False, True):
                 for ur in (False, True):
-                    for store in ("staged", "direct"):
+                    for store in ("auto", "staged", "tma", "direct"):
                         var = fb.make_variant("laplacian", 2, "f32", element_batch_size=bs,
                                               num_concurrent_elements=ce, interleave_stores=is_,
                                               loop_unroll=ur, store=store)
