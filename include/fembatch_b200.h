@@ -20,6 +20,9 @@
  *   fb_build_analytic_tensor <- fembatch::build_analytic_tensor  src/forms.cpp:234-246
  *   fb_structured_mesh /     <- structured_simplicial_mesh /     src/geometry.cpp:164-262
  *   fb_jitter_mesh              jitter_mesh (input synthesis)
+ *   fb_assembly_* /          <- (no reference counterpart: global sparse assembly is the
+ *   fb_assemble                 reference's declared non-goal; it consumes the
+ *                               ElementMatrixStore, include/fembatch/engine.hpp:27-43)
  *
  * Errors: every call returns an fb_status code and, when `err` is non-NULL,
  * fills it with the reference's exception text (same wording as the
@@ -202,6 +205,41 @@ int fb_status_reset(int64_t* status, void* stream, fb_error* err);
 /* Synchronises `stream`, then maps the status words to the reference
  * exception (FB_ERR_RUNTIME "degenerate element: det(J) <= 0 in cell N"). */
 int fb_status_check(const int64_t* status, void* stream, fb_error* err);
+
+/* ---- global assembly (beyond the reference) -----------
+ * CSR matrix of the global operator from an ElementMatrixStore.
+ *   dof(v, c) = v*nc + c, nc = dim for elasticity, 1 otherwise (component c
+ *   of the store's local index i = a + c*(dim+1)).
+ *   Pattern: row (v, c) holds every dof of every vertex sharing an element
+ *   with v (v included), columns ascending; explicit zeros are kept
+ *   (elasticity's off-diagonal component blocks).
+ *   Values: A[r][s] = sum over elements e in ASCENDING order of the store
+ *   entries mapping to (r, s), in engine precision from +0 -- bitwise the
+ *   serial loop "for e: for (i, j): A[dof_i][dof_j] += Ae(i, j)".
+ * The plan (pattern + vertex->element incidence lists) is built on the host
+ * once per mesh; fb_assemble* run one deterministic gather kernel (no
+ * atomics).  Only the real elements (0 .. num_elements-1) of the store are
+ * read; padding slots are ignored. */
+typedef struct fb_assembly fb_assembly;
+
+/* cells: host or device pointer (num_elements*(dim+1) int32).  Errors:
+ * out-of-range vertex id or a repeated vertex within a cell
+ * (FB_ERR_INVALID_ARGUMENT, err->cell = the cell), vertex degree > 255. */
+fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t num_elements,
+                                int64_t num_vertices, fb_error* err);
+void fb_assembly_free(fb_assembly* a);
+int64_t fb_assembly_rows(const fb_assembly* a);
+int64_t fb_assembly_nnz(const fb_assembly* a);
+/* Host copies: row_ptr[rows+1] (int64), col_idx[nnz] (int32). */
+int fb_assembly_pattern(const fb_assembly* a, int64_t* row_ptr, int64_t row_ptr_len,
+                        int32_t* col_idx, int64_t nnz, fb_error* err);
+/* values[nnz] (engine precision of v).  store/values: host or device
+ * pointers (host data is staged through the device of `device`). */
+int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len,
+                void* values, int64_t nnz, int device, fb_error* err);
+/* Device pointers on the current device; enqueued on `stream`. */
+int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* store,
+                      int64_t store_len, void* values, int64_t nnz, void* stream, fb_error* err);
 
 #ifdef __cplusplus
 }

@@ -444,3 +444,154 @@ int64_t fbo_element_matrix_index(int krows, int bs, int ce, int64_t element,
   return batch * nk * bs + (int64_t)(r / ce) * ce * nk + (int64_t)(r % ce) * nk
          + i + (int64_t)j * krows;
 }
+
+/* ------------------------------------------------------------------------
+ * Global assembly.  The reference stops at element
+ * matrices: global sparse assembly is an explicit non-goal, so
+ * there is no reference code to follow.  This is the serial DEFINITION the
+ * GPU assembly is checked against:
+ *   dof(v, c) = v*nc + c, nc = dim for elasticity (component c of the
+ *   reference's local index i = a + c*nb, forms.cpp:175-202) else 1;
+ *   pattern = every (dof_i, dof_j) pair of every element, columns sorted;
+ *   values: for e = 0..ne-1 ascending, for (i, j):
+ *           A[dof_i][dof_j] += Ae[i + j*krows]   (store layout, engine.cpp:287-299)
+ *   in engine precision from +0.
+ * The pattern is built by sorting all element vertex pairs (independent of
+ * the library's vertex-adjacency construction). */
+static int cmp_i64(const void* x, const void* y)
+{
+  const int64_t a = *(const int64_t*)x, b = *(const int64_t*)y;
+  return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+static int asm_nc(int op, int dim) { return op == 1 ? dim : 1; }
+
+/* Sorted unique vertex pairs va*nv + vb of all elements; *npairs. */
+static int64_t* asm_pairs(int dim, const int32_t* cells, int64_t ne, int64_t nv, int64_t* npairs)
+{
+  const int nb = dim + 1;
+  const int64_t n = ne * nb * nb;
+  int64_t* p = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+  if (!p)
+    return NULL;
+  int64_t k = 0;
+  for (int64_t e = 0; e < ne; ++e)
+    for (int a = 0; a < nb; ++a)
+      for (int b = 0; b < nb; ++b)
+        p[k++] = (int64_t)cells[e * nb + a] * nv + cells[e * nb + b];
+  qsort(p, (size_t)n, sizeof(int64_t), cmp_i64);
+  int64_t u = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (u == 0 || p[i] != p[u - 1])
+      p[u++] = p[i];
+  *npairs = u;
+  return p;
+}
+
+static int asm_check_cells(int dim, const int32_t* cells, int64_t ne, int64_t nv)
+{
+  const int nb = dim + 1;
+  for (int64_t e = 0; e < ne; ++e)
+    for (int a = 0; a < nb; ++a)
+    {
+      const int32_t v = cells[e * nb + a];
+      if (v < 0 || v >= nv)
+        return FBO_E_RANGE;
+      for (int b = 0; b < a; ++b)
+        if (cells[e * nb + b] == v)
+          return FBO_E_ARG;
+    }
+  return FBO_OK;
+}
+
+int64_t fbo_assembly_nnz(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv)
+{
+  if ((dim != 2 && dim != 3) || asm_check_cells(dim, cells, ne, nv) != FBO_OK)
+    return -1;
+  int64_t np = 0;
+  int64_t* p = asm_pairs(dim, cells, ne, nv, &np);
+  if (!p)
+    return -1;
+  free(p);
+  const int nc = asm_nc(op, dim);
+  return np * nc * nc;
+}
+
+int fbo_assembly_pattern(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv,
+                         int64_t* row_ptr, int32_t* col_idx)
+{
+  if (dim != 2 && dim != 3)
+    return FBO_E_ARG;
+  const int rc = asm_check_cells(dim, cells, ne, nv);
+  if (rc != FBO_OK)
+    return rc;
+  const int nc = asm_nc(op, dim);
+  int64_t np = 0;
+  int64_t* p = asm_pairs(dim, cells, ne, nv, &np);
+  if (!p)
+    return FBO_E_ARG;
+  /* vertex degree -> row lengths deg*nc for each of the nc rows of a vertex */
+  int64_t* first = (int64_t*)calloc((size_t)nv + 1, sizeof(int64_t));
+  for (int64_t i = 0; i < np; ++i)
+    first[p[i] / nv + 1]++;
+  for (int64_t v = 0; v < nv; ++v)
+    first[v + 1] += first[v]; /* pair range of vertex v */
+  int64_t nz = 0;
+  row_ptr[0] = 0;
+  for (int64_t v = 0; v < nv; ++v)
+    for (int ci = 0; ci < nc; ++ci)
+    {
+      for (int64_t q = first[v]; q < first[v + 1]; ++q)
+        for (int cj = 0; cj < nc; ++cj)
+          col_idx[nz++] = (int32_t)((p[q] % nv) * nc + cj);
+      row_ptr[v * nc + ci + 1] = nz;
+    }
+  free(first);
+  free(p);
+  return FBO_OK;
+}
+
+int fbo_assemble(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv, int precision,
+                 const void* store, const int64_t* row_ptr, const int32_t* col_idx, void* values)
+{
+  if (dim != 2 && dim != 3)
+    return FBO_E_ARG;
+  const int nb = dim + 1, nc = asm_nc(op, dim), kr = nb * nc;
+  const int64_t nk = (int64_t)kr * kr, nnz = row_ptr[nv * nc];
+  if (precision == 0)
+    for (int64_t z = 0; z < nnz; ++z)
+      ((float*)values)[z] = 0.0f;
+  else
+    for (int64_t z = 0; z < nnz; ++z)
+      ((double*)values)[z] = 0.0;
+  for (int64_t e = 0; e < ne; ++e)
+    for (int j = 0; j < kr; ++j)
+      for (int i = 0; i < kr; ++i)
+      {
+        const int64_t row = (int64_t)cells[e * nb + i % nb] * nc + i / nb;
+        const int32_t col = (int32_t)((int64_t)cells[e * nb + j % nb] * nc + j / nb);
+        int64_t lo = row_ptr[row], hi = row_ptr[row + 1];
+        while (lo < hi)
+        {
+          const int64_t mid = lo + (hi - lo) / 2;
+          if (col_idx[mid] < col)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        if (lo >= row_ptr[row + 1] || col_idx[lo] != col)
+          return FBO_E_ARG;
+        const int64_t src = e * nk + i + (int64_t)j * kr;
+        if (precision == 0)
+        {
+          float* a = (float*)values + lo;
+          *a = *a + ((const float*)store)[src];
+        }
+        else
+        {
+          double* a = (double*)values + lo;
+          *a = *a + ((const double*)store)[src];
+        }
+      }
+  return FBO_OK;
+}

@@ -79,6 +79,16 @@ int64_t fbo_flop_count(int op, int dim, int64_t ne);
 int64_t fbo_element_matrix_index(int krows, int bs, int ce, int64_t element,
                                  int i, int j);
 
+/* Global assembly (no reference counterpart: SPEC.md:370 non-goal; the
+ * serial definition the GPU assembly is checked against).  dof = v*nc + c,
+ * nc = dim for elasticity else 1; CSR with sorted columns; values summed in
+ * ascending element order in engine precision from +0. */
+int64_t fbo_assembly_nnz(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv);
+int fbo_assembly_pattern(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv,
+                         int64_t* row_ptr, int32_t* col_idx);
+int fbo_assemble(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv, int precision,
+                 const void* store, const int64_t* row_ptr, const int32_t* col_idx, void* values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,10 @@ class Restatement:
         L.fbo_element_matrix_index.argtypes = [_i32, _i32, _i32, _i64, _i32, _i32]
         L.fbo_element_matrix_index.restype = _i64
         L.fbo_quadrature.argtypes = [_i32, _i32, _vp, _vp]
+        L.fbo_assembly_nnz.argtypes = [_i32, _i32, _vp, _i64, _i64]
+        L.fbo_assembly_nnz.restype = _i64
+        L.fbo_assembly_pattern.argtypes = [_i32, _i32, _vp, _i64, _i64, _vp, _vp]
+        L.fbo_assemble.argtypes = [_i32, _i32, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]
 
     def quadrature(self, dim, degree):
         p = np.zeros(15)
@@ -184,6 +188,33 @@ class Restatement:
 
     def element_matrix_index(self, krows_, bs, ce, e, i, j):
         return self.lib.fbo_element_matrix_index(krows_, bs, ce, e, i, j)
+
+    def assembly_pattern(self, op, dim, cells, nv):
+        """CSR pattern (row_ptr int64, col_idx int32) of the global operator."""
+        c = np.ascontiguousarray(cells, dtype=np.int32)
+        ne = c.size // (dim + 1)
+        nnz = self.lib.fbo_assembly_nnz(op_id(op), dim, _ptr(c), ne, nv)
+        if nnz < 0:
+            raise OracleError("invalid cells for assembly")
+        nc = dim if op_id(op) == 1 else 1
+        row_ptr = np.zeros(nv * nc + 1, dtype=np.int64)
+        col_idx = np.zeros(max(nnz, 1), dtype=np.int32)[:nnz]
+        rc = self.lib.fbo_assembly_pattern(op_id(op), dim, _ptr(c), ne, nv, _ptr(row_ptr), _ptr(col_idx))
+        if rc != 0:
+            raise OracleError(f"assembly_pattern failed ({rc})")
+        return row_ptr, col_idx
+
+    def assemble(self, op, dim, cells, nv, precision, store, row_ptr, col_idx):
+        """CSR values: element matrices of `store` summed in element order."""
+        c = np.ascontiguousarray(cells, dtype=np.int32)
+        ne = c.size // (dim + 1)
+        s = np.ascontiguousarray(store, dtype=scalar_dtype(precision))
+        vals = np.zeros(col_idx.size, dtype=scalar_dtype(precision))
+        rc = self.lib.fbo_assemble(op_id(op), dim, _ptr(c), ne, nv, _prec(precision), _ptr(s),
+                                   _ptr(row_ptr), _ptr(col_idx), _ptr(vals))
+        if rc != 0:
+            raise OracleError(f"assemble failed ({rc})")
+        return vals
 
 
 class Reference:

@@ -27,6 +27,7 @@ from .engine import (  # noqa: F401
     store_length,
     unpack_element_matrix,
 )
+from .assembly import AssemblyPlan, assemble, assembly_plan  # noqa: F401
 from .mesh import jitter_mesh, mesh_prefix, structured_mesh  # noqa: F401
 
 __version__ = "0.1.0"

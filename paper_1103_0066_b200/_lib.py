@@ -59,6 +59,13 @@ SIGNATURES = {
     "fb_integrate_packed_async": (_i32, [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _E]),
     "fb_status_reset": (_i32, [_vp, _vp, _E]),
     "fb_status_check": (_i32, [_vp, _vp, _E]),
+    "fb_assembly_create": (_vp, [_i32, _i32, _vp, _i64, _i64, _E]),
+    "fb_assembly_free": (None, [_vp]),
+    "fb_assembly_rows": (_i64, [_vp]),
+    "fb_assembly_nnz": (_i64, [_vp]),
+    "fb_assembly_pattern": (_i32, [_vp, _vp, _i64, _vp, _i64, _E]),
+    "fb_assemble": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _E]),
+    "fb_assemble_async": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _E]),
 }
 
 _lib = None

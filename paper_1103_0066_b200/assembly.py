@@ -1,0 +1,94 @@
+"""Global CSR assembly from the element-matrix store.
+
+The reference stops at element matrices (global assembly is its declared
+non-goal, ``SPEC.md:370``); this is the consumer a finite-element code puts
+after ``integrate_mesh``.  ``AssemblyPlan`` wraps the C ABI's
+``fb_assembly`` (``include/fembatch_b200.h``, "global assembly"): the CSR
+pattern and vertex->element incidence lists are built once per mesh on the
+host, and ``assemble`` runs one deterministic gather kernel on the GPU whose
+result is bitwise the serial element-order sum.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+from .engine import KernelVariant, _as, _is_torch, _numel, _op, _ptr
+
+
+class AssemblyPlan:
+    """CSR plan of the global operator of ``op`` on a mesh's connectivity.
+
+    dof(v, c) = v*nc + c with nc = dim for elasticity, 1 otherwise.
+    """
+
+    def __init__(self, op: str, dim: int, cells, num_vertices: int):
+        lib = L.load()
+        self.op, self.dim = op, dim
+        cells = _as(cells, np.int32)
+        self.num_elements = _numel(cells) // (dim + 1)
+        self.num_vertices = int(num_vertices)
+        err = L.fb_error()
+        h = lib.fb_assembly_create(_op(op), dim, _ptr(cells), self.num_elements, self.num_vertices,
+                                   C.byref(err))
+        if not h:
+            L.raise_for(err.code or L.FB_ERR_INVALID_ARGUMENT, err)
+        self._h = C.c_void_p(h)
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            self._lib.fb_assembly_free(h)
+            self._h = None
+
+    @property
+    def rows(self) -> int:
+        return self._lib.fb_assembly_rows(self._h)
+
+    @property
+    def nnz(self) -> int:
+        return self._lib.fb_assembly_nnz(self._h)
+
+    def pattern(self):
+        """(row_ptr int64[rows+1], col_idx int32[nnz]) on the host."""
+        row_ptr = np.empty(self.rows + 1, dtype=np.int64)
+        col_idx = np.empty(self.nnz, dtype=np.int32)
+        err = L.fb_error()
+        L.raise_for(self._lib.fb_assembly_pattern(self._h, row_ptr.ctypes.data, row_ptr.size,
+                                                  col_idx.ctypes.data, col_idx.size, C.byref(err)), err)
+        return row_ptr, col_idx
+
+    def assemble(self, variant: KernelVariant, store, values=None, device: int = 0):
+        """CSR values (engine precision) of the element matrices in ``store``."""
+        store = _as(store, variant.dtype)
+        if values is None:
+            if _is_torch(store) and store.is_cuda:
+                import torch
+                values = torch.empty(self.nnz, device=store.device,
+                                     dtype=torch.float32 if variant.dtype == np.float32 else torch.float64)
+            else:
+                values = np.empty(self.nnz, dtype=variant.dtype)
+        err = L.fb_error()
+        rc = self._lib.fb_assemble(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
+                                   _numel(values), device, C.byref(err))
+        L.raise_for(rc, err)
+        return values
+
+    def assemble_async(self, variant: KernelVariant, store, values, stream: int = 0):
+        """Enqueue the assembly kernel on ``stream`` (device tensors only)."""
+        err = L.fb_error()
+        rc = self._lib.fb_assemble_async(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
+                                         _numel(values), C.c_void_p(stream), C.byref(err))
+        L.raise_for(rc, err)
+
+
+def assembly_plan(op: str, dim: int, cells, num_vertices: int) -> AssemblyPlan:
+    return AssemblyPlan(op, dim, cells, num_vertices)
+
+
+def assemble(variant: KernelVariant, plan: AssemblyPlan, store, values=None, device: int = 0):
+    return plan.assemble(variant, store, values, device)

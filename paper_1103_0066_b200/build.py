@@ -29,10 +29,11 @@ CU_SOURCES = [
     "fb_kernels_f64_2d.cu",
     "fb_kernels_f64_3d.cu",
     "fb_pack.cu",
+    "fb_assemble.cu",
 ]
-CPP_SOURCES = ["fb_capi.cpp", "fb_host.cpp", "fembatch_api.cpp"]
+CPP_SOURCES = ["fb_capi.cpp", "fb_assembly.cpp", "fb_host.cpp", "fembatch_api.cpp"]
 CU_HOST_SOURCES = ["fb_tma.cpp"]  # host code that includes the kernel headers (nvcc)
-HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h"]
+HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h", "fb_capi_util.h"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "fembatch_b200.h"),
                   os.path.join(ROOT, "include", "fembatch_b200.hpp")]
 

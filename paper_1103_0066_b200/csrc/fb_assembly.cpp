@@ -1,0 +1,371 @@
+// fb_assembly.cpp -- extern "C" global assembly (include/fembatch_b200.h,
+// "global assembly"): the host-side plan (CSR pattern + vertex->element
+// incidence lists, built once per mesh, multithreaded) and the launch of the
+// deterministic gather kernel (fb_assemble.cu).
+//
+// Plan construction:
+//   1. incidences by counting sort over elements in ascending order, so each
+//      vertex's list is ascending in e (this order IS the summation order);
+//   2. per vertex, the sorted unique vertices of its incident elements (the
+//      row block's columns);
+//   3. per incidence, the neighbour slot of each of the element's vertices.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "fb_capi_util.h"
+#include "fb_internal.h"
+
+using namespace fbc;
+
+namespace {
+
+struct DevPlan {
+  int64_t* v2e_ptr = nullptr;
+  uint32_t* v2e = nullptr;
+  uint8_t* nbrpos = nullptr;
+  int64_t* nbr_ptr = nullptr;
+};
+
+}  // namespace
+
+struct fb_assembly {
+  int op = 0, dim = 2, nb = 3, nc = 1;
+  int64_t nv = 0, ne = 0;
+  std::vector<int64_t> v2e_ptr, nbr_ptr;  // nv + 1 each
+  std::vector<uint32_t> v2e;              // e << 2 | a, ascending e per vertex
+  std::vector<uint8_t> nbrpos;            // nb per incidence
+  std::vector<int32_t> nbr;               // sorted neighbour vertices per vertex
+  mutable std::mutex mu;
+  mutable std::map<int, DevPlan> dev;
+  int64_t rows() const { return nv * nc; }
+  int64_t nnz() const { return nbr_ptr.empty() ? 0 : nbr_ptr[nv] * nc * nc; }
+  ~fb_assembly()
+  {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& [d, p] : dev)
+    {
+      cudaSetDevice(d);
+      cudaFree(p.v2e_ptr);
+      cudaFree(p.v2e);
+      cudaFree(p.nbrpos);
+      cudaFree(p.nbr_ptr);
+    }
+    cudaSetDevice(cur);
+  }
+};
+
+namespace {
+
+template <class F>
+void parallel_for(int64_t n, F&& f)
+{
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>(hw, std::max<int64_t>(1, n / 4096));
+  if (nt <= 1)
+  {
+    f(0, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt, static_cast<int>(t)); });
+  for (auto& x : th)
+    x.join();
+}
+
+void build_plan(fb_assembly& A, const int32_t* cells)
+{
+  const int nb = A.nb;
+  const int64_t nv = A.nv, ne = A.ne;
+  // validation (first offending cell in element order)
+  for (int64_t e = 0; e < ne; ++e)
+    for (int a = 0; a < nb; ++a)
+    {
+      const int32_t v = cells[e * nb + a];
+      if (v < 0 || v >= nv)
+        throw_code(FB_ERR_INVALID_ARGUMENT, "cell vertex index out of range in cell " + std::to_string(e), e);
+      for (int b = 0; b < a; ++b)
+        if (cells[e * nb + b] == v)
+          throw_code(FB_ERR_INVALID_ARGUMENT, "repeated vertex in cell " + std::to_string(e), e);
+    }
+  // 1. incidences, ascending e per vertex
+  A.v2e_ptr.assign(nv + 1, 0);
+  for (int64_t i = 0; i < ne * nb; ++i)
+    A.v2e_ptr[cells[i] + 1]++;
+  for (int64_t v = 0; v < nv; ++v)
+    A.v2e_ptr[v + 1] += A.v2e_ptr[v];
+  A.v2e.resize(ne * nb);
+  {
+    std::vector<int64_t> fill(A.v2e_ptr.begin(), A.v2e_ptr.end() - 1);
+    for (int64_t e = 0; e < ne; ++e)
+      for (int a = 0; a < nb; ++a)
+        A.v2e[fill[cells[e * nb + a]]++] = static_cast<uint32_t>(e << 2 | a);
+  }
+  // 2. neighbour lists (per thread chunk, then concatenated)
+  std::vector<std::vector<int32_t>> chunk_nbr(std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<int64_t> deg(nv, 0);
+  std::vector<int64_t> chunk_lo(chunk_nbr.size(), -1);
+  parallel_for(nv,
+               [&](int64_t v0, int64_t v1, int t)
+               {
+                 std::vector<int32_t> tmp;
+                 auto& out = chunk_nbr[t];
+                 chunk_lo[t] = v0;
+                 for (int64_t v = v0; v < v1; ++v)
+                 {
+                   tmp.clear();
+                   for (int64_t q = A.v2e_ptr[v]; q < A.v2e_ptr[v + 1]; ++q)
+                   {
+                     const int64_t e = A.v2e[q] >> 2;
+                     for (int b = 0; b < nb; ++b)
+                       tmp.push_back(cells[e * nb + b]);
+                   }
+                   std::sort(tmp.begin(), tmp.end());
+                   tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+                   deg[v] = static_cast<int64_t>(tmp.size());
+                   out.insert(out.end(), tmp.begin(), tmp.end());
+                 }
+               });
+  A.nbr_ptr.assign(nv + 1, 0);
+  for (int64_t v = 0; v < nv; ++v)
+  {
+    if (deg[v] > 255)
+      throw_code(FB_ERR_INVALID_ARGUMENT, "vertex degree exceeds 255 at vertex " + std::to_string(v), -1);
+    A.nbr_ptr[v + 1] = A.nbr_ptr[v] + deg[v];
+  }
+  A.nbr.resize(A.nbr_ptr[nv]);
+  {
+    std::vector<std::pair<int64_t, size_t>> order;
+    for (size_t t = 0; t < chunk_nbr.size(); ++t)
+      if (chunk_lo[t] >= 0)
+        order.push_back({chunk_lo[t], t});
+    std::sort(order.begin(), order.end());
+    for (auto& [lo, t] : order)
+      std::copy(chunk_nbr[t].begin(), chunk_nbr[t].end(), A.nbr.begin() + A.nbr_ptr[lo]);
+  }
+  if (A.nbr_ptr[nv] * A.nc > INT32_MAX || A.rows() > INT32_MAX)
+    throw_code(FB_ERR_INVALID_ARGUMENT, "assembled operator exceeds 32-bit column indices", -1);
+  // 3. neighbour slot of every local vertex of every incidence
+  A.nbrpos.resize(ne * nb * nb);
+  parallel_for(nv,
+               [&](int64_t v0, int64_t v1, int)
+               {
+                 for (int64_t v = v0; v < v1; ++v)
+                 {
+                   const int32_t* lo = A.nbr.data() + A.nbr_ptr[v];
+                   const int32_t* hi = A.nbr.data() + A.nbr_ptr[v + 1];
+                   for (int64_t q = A.v2e_ptr[v]; q < A.v2e_ptr[v + 1]; ++q)
+                   {
+                     const int64_t e = A.v2e[q] >> 2;
+                     for (int b = 0; b < nb; ++b)
+                       A.nbrpos[q * nb + b] =
+                           static_cast<uint8_t>(std::lower_bound(lo, hi, cells[e * nb + b]) - lo);
+                   }
+                 }
+               });
+}
+
+template <class T>
+T* upload(const std::vector<T>& h)
+{
+  T* d = nullptr;
+  cuda_check(cudaMalloc(&d, std::max<size_t>(h.size(), 1) * sizeof(T)), "cudaMalloc");
+  if (!h.empty())
+    cuda_check(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy plan");
+  return d;
+}
+
+const DevPlan& plan_on(const fb_assembly& A, int dev)
+{
+  std::lock_guard<std::mutex> lock(A.mu);
+  auto it = A.dev.find(dev);
+  if (it != A.dev.end())
+    return it->second;
+  DevPlan p;
+  p.v2e_ptr = upload(A.v2e_ptr);
+  p.v2e = upload(A.v2e);
+  p.nbrpos = upload(A.nbrpos);
+  p.nbr_ptr = upload(A.nbr_ptr);
+  return A.dev.emplace(dev, p).first->second;
+}
+
+void check_pair(const fb_assembly* a, const fb_variant* v, int64_t store_len, int64_t nnz)
+{
+  if (!a)
+    invalid("null assembly plan");
+  if (!v)
+    invalid("null kernel variant");
+  if (v->dim != a->dim)
+    invalid("assembly plan and variant differ in dimension");
+  if ((v->op == FB_ELASTICITY) != (a->op == FB_ELASTICITY))
+    invalid("assembly plan and variant differ in operator shape");
+  if (store_len < a->ne * v->krows * v->krows)
+    invalid("element matrix store shorter than num_elements * krows^2");
+  if (nnz != a->nnz())
+    invalid("values length must equal the plan's nnz");
+}
+
+void launch_on(const fb_assembly& A, const fb_variant& v, const void* store, void* values, int dev,
+               cudaStream_t st)
+{
+  const DevPlan& p = plan_on(A, dev);
+  fbk::AsmArgs g;
+  g.v2e_ptr = p.v2e_ptr;
+  g.v2e = p.v2e;
+  g.nbrpos = p.nbrpos;
+  g.nbr_ptr = p.nbr_ptr;
+  g.store = store;
+  g.values = values;
+  g.nv = A.nv;
+  cuda_check(fbk::launch_assemble(A.dim, A.nc, v.cfg.precision, g, st), "assemble kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t ne, int64_t nv, fb_error* err)
+{
+  std::unique_ptr<fb_assembly> A;
+  const int rc = guarded(err,
+                         [&]
+                         {
+                           if (dim != 2 && dim != 3)
+                             invalid("unsupported spatial dimension " + std::to_string(dim));
+                           if (op < FB_LAPLACIAN || op > FB_WEIGHTED_LAPLACIAN)
+                             invalid("unknown operator");
+                           if (ne < 0 || nv < 0 || nv > INT32_MAX || ne >= (int64_t(1) << 30))
+                             invalid("mesh sizes out of range for assembly");
+                           if (ne > 0 && !cells)
+                             invalid("null cells");
+                           A = std::make_unique<fb_assembly>();
+                           A->op = op;
+                           A->dim = dim;
+                           A->nb = dim + 1;
+                           A->nc = op == FB_ELASTICITY ? dim : 1;
+                           A->nv = nv;
+                           A->ne = ne;
+                           std::vector<int32_t> host;
+                           const int32_t* c = cells;
+                           if (ne > 0 && pointer_device(cells) >= 0)
+                           {
+                             host.resize(ne * (dim + 1));
+                             cuda_check(cudaMemcpy(host.data(), cells, host.size() * sizeof(int32_t),
+                                                   cudaMemcpyDeviceToHost),
+                                        "cudaMemcpy cells");
+                             c = host.data();
+                           }
+                           build_plan(*A, c);
+                         });
+  return rc == FB_OK ? A.release() : nullptr;
+}
+
+void fb_assembly_free(fb_assembly* a) { delete a; }
+int64_t fb_assembly_rows(const fb_assembly* a) { return a ? a->rows() : -1; }
+int64_t fb_assembly_nnz(const fb_assembly* a) { return a ? a->nnz() : -1; }
+
+int fb_assembly_pattern(const fb_assembly* a, int64_t* row_ptr, int64_t row_ptr_len, int32_t* col_idx,
+                        int64_t nnz, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   if (!a)
+                     invalid("null assembly plan");
+                   if (row_ptr_len != a->rows() + 1 || nnz != a->nnz())
+                     invalid("pattern buffers must hold rows+1 offsets and nnz columns");
+                   const int nc = a->nc;
+                   int64_t z = 0;
+                   row_ptr[0] = 0;
+                   for (int64_t v = 0; v < a->nv; ++v)
+                     for (int ci = 0; ci < nc; ++ci)
+                     {
+                       for (int64_t k = a->nbr_ptr[v]; k < a->nbr_ptr[v + 1]; ++k)
+                         for (int cj = 0; cj < nc; ++cj)
+                           col_idx[z++] = static_cast<int32_t>(a->nbr[k] * nc + cj);
+                       row_ptr[v * nc + ci + 1] = z;
+                     }
+                 });
+}
+
+int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len,
+                      void* values, int64_t nnz, void* stream, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   check_pair(a, v, store_len, nnz);
+                   int dev = 0;
+                   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+                   launch_on(*a, *v, store, values, dev, static_cast<cudaStream_t>(stream));
+                 });
+}
+
+int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len, void* values,
+                int64_t nnz, int device, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   check_pair(a, v, store_len, nnz);
+                   if (device_count() == 0)
+                     throw_code(FB_ERR_NO_DEVICE, "no CUDA device available");
+                   const int sdev = pointer_device(store), vdev = pointer_device(values);
+                   const int dev = sdev >= 0 ? sdev : (vdev >= 0 ? vdev : std::max(device, 0));
+                   int cur = 0;
+                   cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+                   cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+                   const size_t ss = scalar_size(v->cfg.precision);
+                   const size_t sbytes = static_cast<size_t>(a->ne) * v->krows * v->krows * ss;
+                   const size_t vbytes = static_cast<size_t>(nnz) * ss;
+                   void* ds = const_cast<void*>(store);
+                   void* dv = values;
+                   void* tmp_s = nullptr;
+                   void* tmp_v = nullptr;
+                   cudaStream_t st = nullptr;
+                   try
+                   {
+                     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+                     if (sdev != dev)
+                     {
+                       cuda_check(cudaMalloc(&tmp_s, std::max<size_t>(sbytes, 16)), "cudaMalloc");
+                       cuda_check(cudaMemcpyAsync(tmp_s, store, sbytes, cudaMemcpyDefault, st), "upload store");
+                       ds = tmp_s;
+                     }
+                     if (vdev != dev)
+                     {
+                       cuda_check(cudaMalloc(&tmp_v, std::max<size_t>(vbytes, 16)), "cudaMalloc");
+                       dv = tmp_v;
+                     }
+                     launch_on(*a, *v, ds, dv, dev, st);
+                     if (tmp_v)
+                       cuda_check(cudaMemcpyAsync(values, tmp_v, vbytes, cudaMemcpyDefault, st), "download values");
+                     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+                   }
+                   catch (...)
+                   {
+                     if (st)
+                       cudaStreamSynchronize(st);
+                     cudaFree(tmp_s);
+                     cudaFree(tmp_v);
+                     if (st)
+                       cudaStreamDestroy(st);
+                     cudaSetDevice(cur);
+                     throw;
+                   }
+                   cudaFree(tmp_s);
+                   cudaFree(tmp_v);
+                   cudaStreamDestroy(st);
+                   cudaSetDevice(cur);
+                 });
+}
+
+}  // extern "C"

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/fembatch_b200.h"
+#include "fb_capi_util.h"
 #include "fb_host.h"
 #include "fb_internal.h"
 
@@ -32,98 +33,11 @@ namespace fbk {
 std::atomic<long long>& launch_counter();
 }
 
-struct fb_variant {
-  int op = 0, dim = 2, nb = 3, krows = 3, ncoef = 1;
-  fb_kernel_config cfg{};
-  int path = fbk::kDense;
-  std::string description;
-  std::vector<double> k;                   // AnalyticTensor doubles as given
-  fbk::KParamBlob kp{};                    // sparse block, engine precision
-  std::vector<unsigned char> kdense;       // dense K, engine precision
-  mutable std::mutex mu;
-  mutable std::map<int, void*> kdense_dev;  // per device (dense path only)
-  ~fb_variant()
-  {
-    for (auto& [dev, p] : kdense_dev)
-    {
-      int cur = 0;
-      cudaGetDevice(&cur);
-      cudaSetDevice(dev);
-      cudaFree(p);
-      cudaSetDevice(cur);
-    }
-  }
-};
-
 namespace {
 
+using namespace fbc;
+
 constexpr long long kStatusInit = 0x7f7f7f7f7f7f7f7fLL;  // memset(0x7f) pattern
-
-// ---------------------------------------------------------------- errors
-struct Error {
-  int code;
-  std::string msg;
-  int64_t cell;
-};
-
-[[noreturn]] void throw_code(int code, const std::string& msg, int64_t cell = -1)
-{
-  throw Error{code, msg, cell};
-}
-
-[[noreturn]] void invalid(const std::string& msg) { throw_code(FB_ERR_INVALID_ARGUMENT, msg); }
-
-void cuda_check(cudaError_t e, const char* what)
-{
-  if (e != cudaSuccess)
-    throw_code(FB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-void fill_err(fb_error* err, int code, const std::string& msg, int64_t cell)
-{
-  if (!err)
-    return;
-  err->code = code;
-  err->reserved = 0;
-  err->cell = cell;
-  std::snprintf(err->message, sizeof err->message, "%s", msg.c_str());
-}
-
-template <class F>
-int guarded(fb_error* err, F&& f)
-{
-  try
-  {
-    f();
-    fill_err(err, FB_OK, "", -1);
-    return FB_OK;
-  }
-  catch (const Error& e)
-  {
-    fill_err(err, e.code, e.msg, e.cell);
-    return e.code;
-  }
-  catch (const std::invalid_argument& e)
-  {
-    fill_err(err, FB_ERR_INVALID_ARGUMENT, e.what(), -1);
-    return FB_ERR_INVALID_ARGUMENT;
-  }
-  catch (const std::out_of_range& e)
-  {
-    fill_err(err, FB_ERR_OUT_OF_RANGE, e.what(), -1);
-    return FB_ERR_OUT_OF_RANGE;
-  }
-  catch (const std::bad_alloc&)
-  {
-    fill_err(err, FB_ERR_RUNTIME, "host allocation failed", -1);
-    return FB_ERR_RUNTIME;
-  }
-  catch (const std::exception& e)
-  {
-    fill_err(err, FB_ERR_RUNTIME, e.what(), -1);
-    return FB_ERR_RUNTIME;
-  }
-}
 
 // ----------------------------------------------------- config validation
 // src/kernel_config.cpp:43-55
@@ -150,7 +64,6 @@ int64_t store_len(int krows, int64_t ne, int bs)
   return nbatch * bs * static_cast<int64_t>(krows) * krows;
 }
 
-size_t scalar_size(int prec) { return prec == FB_F32 ? 4 : 8; }
 
 // ------------------------------------------------- K structure analysis
 template <class S>
@@ -281,33 +194,6 @@ DeviceCtx& ctx_for(int dev)
   if (it == m.end())
     it = m.emplace(dev, std::make_unique<DeviceCtx>()).first;
   return *it->second;
-}
-
-int device_count()
-{
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess)
-  {
-    cudaGetLastError();
-    return 0;
-  }
-  return n;
-}
-
-// Memory kind of a pointer: -1 host (pageable or pinned), else device id.
-int pointer_device(const void* p)
-{
-  if (!p)
-    return -1;
-  cudaPointerAttributes attr{};
-  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess)
-  {
-    cudaGetLastError();
-    return -1;
-  }
-  if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)
-    return attr.device;
-  return -1;
 }
 
 const void* kdense_on(const fb_variant& v, int dev)

@@ -1,0 +1,110 @@
+"""Global CSR assembly on the GPU: the gather kernel's
+values are BITWISE the oracle's serial element-order sum over the same store
+(every op x dim x precision, host and device buffers, the async API), and at
+a BASELINE size the assembled operator keeps the size-independent properties
+(bitwise symmetry, zero Laplacian row sums, translation null space)."""
+import numpy as np
+import pytest
+
+import paper_1103_0066_b200 as fb
+from paper_1103_0066_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+OPS = ["laplacian", "elasticity", "weighted-laplacian"]
+
+
+def coeffs_for(op, v, c, dim):
+    if op != "weighted-laplacian":
+        return None
+    return np.ascontiguousarray(1.0 + v.reshape(-1, dim)[c.reshape(-1, dim + 1), 0].ravel())
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("dim,n", [(2, 9), (3, 4)])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_assembly_bitwise_vs_oracle(restatement, op, dim, n, prec):
+    import torch
+
+    v, c = fb.structured_mesh(dim, n, 0.15, 42)
+    nv = v.size // dim
+    w = coeffs_for(op, v, c, dim)
+    var = fb.make_variant(op, dim, prec, "strict", element_batch_size=16)
+    store = fb.integrate_mesh(var, v, c, w)  # host in, host out (padded store)
+    want_store = restatement.integrate_mesh(op, v, c, dim, bs=16, precision=prec, coeffs=w)
+    assert store.tobytes() == want_store.tobytes()
+    plan = fb.AssemblyPlan(op, dim, c, nv)
+    rp, ci = plan.pattern()
+    want = restatement.assemble(op, dim, c, nv, prec, want_store, rp, ci)
+    got_host = plan.assemble(var, store)
+    assert got_host.tobytes() == want.tobytes()
+    dstore = torch.from_numpy(store).cuda()
+    got_dev = plan.assemble(var, dstore)
+    assert got_dev.is_cuda and got_dev.cpu().numpy().tobytes() == want.tobytes()
+    vals = torch.full((plan.nnz,), float("nan"), dtype=dstore.dtype, device="cuda")
+    plan.assemble_async(var, dstore, vals, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert vals.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_assembly_shuffled_cells_and_unreferenced_vertices(restatement):
+    v, c, _ = fb.mesh_prefix(3, 1000, 0.1)
+    nv = v.size // 3
+    cs = c.reshape(-1, 4)[np.random.default_rng(3).permutation(1000)].ravel().copy()
+    for cells in (c, cs):
+        var = fb.make_variant("elasticity", 3, "f32", "strict", element_batch_size=128)
+        store = fb.integrate_mesh(var, v, cells)
+        plan = fb.AssemblyPlan("elasticity", 3, cells, nv)
+        rp, ci = plan.pattern()
+        want = restatement.assemble("elasticity", 3, cells, nv, "f32", store, rp, ci)
+        assert plan.assemble(var, store).tobytes() == want.tobytes()
+
+
+def test_assembly_validation():
+    import torch
+
+    v, c = fb.structured_mesh(2, 4)
+    nv = v.size // 2
+    plan = fb.AssemblyPlan("laplacian", 2, c, nv)
+    var = fb.make_variant("laplacian", 2, "f64", element_batch_size=1)
+    store = fb.integrate_mesh(var, v, c)
+    with pytest.raises(_lib.InvalidArgument, match="nnz"):
+        plan.assemble(var, store, np.empty(plan.nnz + 1))
+    with pytest.raises(_lib.InvalidArgument, match="shorter"):
+        plan.assemble(var, store[:-1])
+    with pytest.raises(_lib.InvalidArgument, match="operator shape"):
+        plan.assemble(fb.make_variant("elasticity", 2, "f64", element_batch_size=1),
+                      np.zeros(c.size // 3 * 36))
+    with pytest.raises(_lib.InvalidArgument, match="dimension"):
+        plan.assemble(fb.make_variant("laplacian", 3, "f64", element_batch_size=1), np.zeros(10 ** 4))
+    del torch
+
+
+@pytest.mark.parametrize("op,dim,ne,prec", [("laplacian", 3, 1 << 22, "f32"), ("elasticity", 2, 1 << 20, "f32"),
+                                            ("elasticity", 3, 1 << 19, "f64")])
+def test_assembly_properties_at_size(op, dim, ne, prec):
+    import torch
+
+    v, c, _ = fb.mesh_prefix(dim, ne, 0.15 if ne <= (1 << 22) else 0.0)
+    nv = v.size // dim
+    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+    var = fb.make_variant(op, dim, prec, "strict")
+    store = fb.integrate_mesh(var, dv, dc)
+    plan = fb.AssemblyPlan(op, dim, c, nv)
+    vals = plan.assemble(var, store)
+    rp, ci = plan.pattern()
+    rows = torch.repeat_interleave(torch.arange(plan.rows, device="cuda"), torch.from_numpy(np.diff(rp)).cuda())
+    cols = torch.from_numpy(ci).cuda().long()
+    # bitwise symmetry: A[r, c] == A[c, r] for every stored entry
+    key = rows * plan.rows + cols
+    tkey = cols * plan.rows + rows
+    order = torch.argsort(key)
+    pos = torch.searchsorted(key[order], tkey)
+    assert torch.equal(key[order][pos], tkey)
+    assert torch.equal(vals[order][pos], vals)
+    scale = vals.abs().max().item()
+    nc = dim if op == "elasticity" else 1
+    v64 = vals.double()
+    for comp in range(nc):
+        t = (cols % nc == comp).double()  # translation in component `comp`
+        r = torch.zeros(plan.rows, dtype=torch.float64, device="cuda").index_add_(0, rows, v64 * t)
+        assert r.abs().max().item() <= (1e-4 if prec == "f32" else 1e-12) * scale
