@@ -233,13 +233,19 @@ int64_t fb_assembly_nnz(const fb_assembly* a);
 /* Host copies: row_ptr[rows+1] (int64), col_idx[nnz] (int32). */
 int fb_assembly_pattern(const fb_assembly* a, int64_t* row_ptr, int64_t row_ptr_len,
                         int32_t* col_idx, int64_t nnz, fb_error* err);
+/* flags: FB_ASSEMBLE_SYMMETRIC = the caller promises every element matrix
+ * in the store is bitwise symmetric (true of fb_integrate_mesh output of a
+ * variant whose fb_variant_path is 0 or 3); the kernel then reads each
+ * needed row as the contiguous column.  Values are identical either way. */
+enum fb_assemble_flags { FB_ASSEMBLE_SYMMETRIC = 1 };
 /* values[nnz] (engine precision of v).  store/values: host or device
  * pointers (host data is staged through the device of `device`). */
 int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len,
-                void* values, int64_t nnz, int device, fb_error* err);
+                void* values, int64_t nnz, int flags, int device, fb_error* err);
 /* Device pointers on the current device; enqueued on `stream`. */
 int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* store,
-                      int64_t store_len, void* values, int64_t nnz, void* stream, fb_error* err);
+                      int64_t store_len, void* values, int64_t nnz, int flags, void* stream,
+                      fb_error* err);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,8 @@ import numpy as np
 from . import _lib as L
 from .engine import KernelVariant, _as, _is_torch, _numel, _op, _ptr
 
+FB_ASSEMBLE_SYMMETRIC = 1
+
 
 class AssemblyPlan:
     """CSR plan of the global operator of ``op`` on a mesh's connectivity.
@@ -62,8 +64,12 @@ class AssemblyPlan:
                                                   col_idx.ctypes.data, col_idx.size, C.byref(err)), err)
         return row_ptr, col_idx
 
-    def assemble(self, variant: KernelVariant, store, values=None, device: int = 0):
-        """CSR values (engine precision) of the element matrices in ``store``."""
+    def assemble(self, variant: KernelVariant, store, values=None, device: int = 0, symmetric: bool = False):
+        """CSR values (engine precision) of the element matrices in ``store``.
+
+        ``symmetric=True`` promises bitwise-symmetric element matrices (the
+        ``integrate_mesh`` output of a variant with ``path`` 0 or 3): rows are
+        then read as contiguous columns.  The values do not depend on it."""
         store = _as(store, variant.dtype)
         if values is None:
             if _is_torch(store) and store.is_cuda:
@@ -74,15 +80,17 @@ class AssemblyPlan:
                 values = np.empty(self.nnz, dtype=variant.dtype)
         err = L.fb_error()
         rc = self._lib.fb_assemble(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
-                                   _numel(values), device, C.byref(err))
+                                   _numel(values), FB_ASSEMBLE_SYMMETRIC if symmetric else 0, device,
+                                   C.byref(err))
         L.raise_for(rc, err)
         return values
 
-    def assemble_async(self, variant: KernelVariant, store, values, stream: int = 0):
+    def assemble_async(self, variant: KernelVariant, store, values, stream: int = 0, symmetric: bool = False):
         """Enqueue the assembly kernel on ``stream`` (device tensors only)."""
         err = L.fb_error()
         rc = self._lib.fb_assemble_async(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
-                                         _numel(values), C.c_void_p(stream), C.byref(err))
+                                         _numel(values), FB_ASSEMBLE_SYMMETRIC if symmetric else 0,
+                                         C.c_void_p(stream), C.byref(err))
         L.raise_for(rc, err)
 
 
@@ -90,5 +98,6 @@ def assembly_plan(op: str, dim: int, cells, num_vertices: int) -> AssemblyPlan:
     return AssemblyPlan(op, dim, cells, num_vertices)
 
 
-def assemble(variant: KernelVariant, plan: AssemblyPlan, store, values=None, device: int = 0):
-    return plan.assemble(variant, store, values, device)
+def assemble(variant: KernelVariant, plan: AssemblyPlan, store, values=None, device: int = 0,
+             symmetric: bool = False):
+    return plan.assemble(variant, store, values, device, symmetric)

@@ -27,9 +27,9 @@ using namespace fbc;
 namespace {
 
 struct DevPlan {
-  int64_t* v2e_ptr = nullptr;
-  uint32_t* v2e = nullptr;
-  uint8_t* nbrpos = nullptr;
+  int64_t* goff = nullptr;
+  uint32_t* spk = nullptr;
+  uint32_t* spos = nullptr;
   int64_t* nbr_ptr = nullptr;
 };
 
@@ -42,6 +42,9 @@ struct fb_assembly {
   std::vector<uint32_t> v2e;              // e << 2 | a, ascending e per vertex
   std::vector<uint8_t> nbrpos;            // nb per incidence
   std::vector<int32_t> nbr;               // sorted neighbour vertices per vertex
+  // device layout (SELL-32, fb_internal.h AsmArgs)
+  std::vector<int64_t> goff;
+  std::vector<uint32_t> spk, spos;
   mutable std::mutex mu;
   mutable std::map<int, DevPlan> dev;
   int64_t rows() const { return nv * nc; }
@@ -53,9 +56,9 @@ struct fb_assembly {
     for (auto& [d, p] : dev)
     {
       cudaSetDevice(d);
-      cudaFree(p.v2e_ptr);
-      cudaFree(p.v2e);
-      cudaFree(p.nbrpos);
+      cudaFree(p.goff);
+      cudaFree(p.spk);
+      cudaFree(p.spos);
       cudaFree(p.nbr_ptr);
     }
     cudaSetDevice(cur);
@@ -171,6 +174,34 @@ void build_plan(fb_assembly& A, const int32_t* cells)
                    }
                  }
                });
+  // 4. sliced (SELL-32) copy for coalesced warp loads: incidence k of vertex
+  //    32g + l at goff[g] + 32k + l
+  const int64_t ngroups = (nv + 31) / 32;
+  A.goff.assign(ngroups + 1, 0);
+  for (int64_t g = 0; g < ngroups; ++g)
+  {
+    int64_t w = 0;
+    for (int64_t v = g * 32; v < std::min(nv, g * 32 + 32); ++v)
+      w = std::max(w, A.v2e_ptr[v + 1] - A.v2e_ptr[v]);
+    A.goff[g + 1] = A.goff[g] + 32 * w;
+  }
+  A.spk.assign(A.goff[ngroups], 0xffffffffu);
+  A.spos.assign(A.goff[ngroups], 0u);
+  parallel_for(ngroups,
+               [&](int64_t g0, int64_t g1, int)
+               {
+                 for (int64_t g = g0; g < g1; ++g)
+                   for (int64_t v = g * 32; v < std::min(nv, g * 32 + 32); ++v)
+                     for (int64_t q = A.v2e_ptr[v]; q < A.v2e_ptr[v + 1]; ++q)
+                     {
+                       const int64_t at = A.goff[g] + 32 * (q - A.v2e_ptr[v]) + (v - g * 32);
+                       A.spk[at] = A.v2e[q];
+                       uint32_t w = 0;
+                       for (int b = 0; b < nb; ++b)
+                         w |= static_cast<uint32_t>(A.nbrpos[q * nb + b]) << (8 * b);
+                       A.spos[at] = w;
+                     }
+               });
 }
 
 template <class T>
@@ -190,9 +221,9 @@ const DevPlan& plan_on(const fb_assembly& A, int dev)
   if (it != A.dev.end())
     return it->second;
   DevPlan p;
-  p.v2e_ptr = upload(A.v2e_ptr);
-  p.v2e = upload(A.v2e);
-  p.nbrpos = upload(A.nbrpos);
+  p.goff = upload(A.goff);
+  p.spk = upload(A.spk);
+  p.spos = upload(A.spos);
   p.nbr_ptr = upload(A.nbr_ptr);
   return A.dev.emplace(dev, p).first->second;
 }
@@ -213,18 +244,26 @@ void check_pair(const fb_assembly* a, const fb_variant* v, int64_t store_len, in
     invalid("values length must equal the plan's nnz");
 }
 
-void launch_on(const fb_assembly& A, const fb_variant& v, const void* store, void* values, int dev,
+void check_flags(int flags)
+{
+  if (flags & ~FB_ASSEMBLE_SYMMETRIC)
+    invalid("unknown assembly flags");
+}
+
+void launch_on(const fb_assembly& A, const fb_variant& v, const void* store, void* values, int flags, int dev,
                cudaStream_t st)
 {
   const DevPlan& p = plan_on(A, dev);
   fbk::AsmArgs g;
-  g.v2e_ptr = p.v2e_ptr;
-  g.v2e = p.v2e;
-  g.nbrpos = p.nbrpos;
+  g.goff = p.goff;
+  g.spk = p.spk;
+  g.spos = p.spos;
   g.nbr_ptr = p.nbr_ptr;
   g.store = store;
   g.values = values;
   g.nv = A.nv;
+  // column reads need the caller's symmetry promise and 16-byte alignment
+  g.sym = (flags & FB_ASSEMBLE_SYMMETRIC) && (reinterpret_cast<uintptr_t>(store) & 15u) == 0 ? 1 : 0;
   cuda_check(fbk::launch_assemble(A.dim, A.nc, v.cfg.precision, g, st), "assemble kernel launch");
 }
 
@@ -297,25 +336,27 @@ int fb_assembly_pattern(const fb_assembly* a, int64_t* row_ptr, int64_t row_ptr_
 }
 
 int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len,
-                      void* values, int64_t nnz, void* stream, fb_error* err)
+                      void* values, int64_t nnz, int flags, void* stream, fb_error* err)
 {
   return guarded(err,
                  [&]
                  {
                    check_pair(a, v, store_len, nnz);
+                   check_flags(flags);
                    int dev = 0;
                    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-                   launch_on(*a, *v, store, values, dev, static_cast<cudaStream_t>(stream));
+                   launch_on(*a, *v, store, values, flags, dev, static_cast<cudaStream_t>(stream));
                  });
 }
 
 int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len, void* values,
-                int64_t nnz, int device, fb_error* err)
+                int64_t nnz, int flags, int device, fb_error* err)
 {
   return guarded(err,
                  [&]
                  {
                    check_pair(a, v, store_len, nnz);
+                   check_flags(flags);
                    if (device_count() == 0)
                      throw_code(FB_ERR_NO_DEVICE, "no CUDA device available");
                    const int sdev = pointer_device(store), vdev = pointer_device(values);
@@ -345,7 +386,7 @@ int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, in
                        cuda_check(cudaMalloc(&tmp_v, std::max<size_t>(vbytes, 16)), "cudaMalloc");
                        dv = tmp_v;
                      }
-                     launch_on(*a, *v, ds, dv, dev, st);
+                     launch_on(*a, *v, ds, dv, flags, dev, st);
                      if (tmp_v)
                        cuda_check(cudaMemcpyAsync(values, tmp_v, vbytes, cudaMemcpyDefault, st), "download values");
                      cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");

@@ -65,19 +65,23 @@ cudaError_t launch_integrate_f64_3d(const LaunchSpec&, const LaunchArgs&, const 
 cudaError_t launch_pack(int dim, int prec, const LaunchArgs&, cudaStream_t);
 
 // Global assembly (fb_assemble.cu): the device half of an fb_assembly plan.
-// Vertex v owns rows (v, c), c < nc; its incidences q in [v2e_ptr[v],
-// v2e_ptr[v+1]) are packed (e << 2 | a), ascending in e, with nbrpos[q*nb + b]
-// = the slot of the element's local vertex b in v's sorted neighbour list
-// [nbr_ptr[v], nbr_ptr[v+1]).  Row (v, ci) starts at value index
-// nbr_ptr[v]*nc^2 + ci*deg*nc; neighbour slot k, component cj at + k*nc + cj.
+// Vertices are taken in groups of 32 (one warp); a group's incidence lists
+// are stored sliced (SELL-32): incidence k of vertex 32g + l at
+// goff[g] + 32k + l, k < (goff[g+1] - goff[g]) / 32, packed (e << 2 | a)
+// ascending in e, padding 0xffffffff; spos at the same index packs the
+// neighbour slot of each of the element's nb local vertices (one byte each)
+// in v's sorted neighbour list [nbr_ptr[v], nbr_ptr[v+1]).  Row (v, ci)
+// starts at value index nbr_ptr[v]*nc^2 + ci*deg*nc; neighbour slot k,
+// component cj at + k*nc + cj.
 struct AsmArgs {
-  const int64_t* v2e_ptr = nullptr;
-  const uint32_t* v2e = nullptr;
-  const uint8_t* nbrpos = nullptr;
-  const int64_t* nbr_ptr = nullptr;
-  const void* store = nullptr;  // element matrices, e*krows^2 + i + j*krows
-  void* values = nullptr;       // CSR values (engine precision)
+  const int64_t* goff = nullptr;    // ngroups + 1
+  const uint32_t* spk = nullptr;    // sliced incidences
+  const uint32_t* spos = nullptr;   // sliced neighbour slots
+  const int64_t* nbr_ptr = nullptr; // nv + 1
+  const void* store = nullptr;      // element matrices, e*krows^2 + i + j*krows
+  void* values = nullptr;           // CSR values (engine precision)
   int64_t nv = 0;
+  int sym = 0;                      // element matrices bitwise symmetric: read columns
 };
 cudaError_t launch_assemble(int dim, int nc, int prec, const AsmArgs&, cudaStream_t);
 

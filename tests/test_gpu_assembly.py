@@ -3,6 +3,8 @@ values are BITWISE the oracle's serial element-order sum over the same store
 (every op x dim x precision, host and device buffers, the async API), and at
 a BASELINE size the assembled operator keeps the size-independent properties
 (bitwise symmetry, zero Laplacian row sums, translation null space)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -35,15 +37,34 @@ def test_assembly_bitwise_vs_oracle(restatement, op, dim, n, prec):
     plan = fb.AssemblyPlan(op, dim, c, nv)
     rp, ci = plan.pattern()
     want = restatement.assemble(op, dim, c, nv, prec, want_store, rp, ci)
-    got_host = plan.assemble(var, store)
-    assert got_host.tobytes() == want.tobytes()
-    dstore = torch.from_numpy(store).cuda()
-    got_dev = plan.assemble(var, dstore)
-    assert got_dev.is_cuda and got_dev.cpu().numpy().tobytes() == want.tobytes()
-    vals = torch.full((plan.nnz,), float("nan"), dtype=dstore.dtype, device="cuda")
-    plan.assemble_async(var, dstore, vals, torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    assert vals.cpu().numpy().tobytes() == want.tobytes()
+    assert var.path in (0, 3)  # symmetric kernel path: element matrices bitwise symmetric
+    for sym in (False, True):
+        got_host = plan.assemble(var, store, symmetric=sym)
+        assert got_host.tobytes() == want.tobytes()
+        dstore = torch.from_numpy(store).cuda()
+        got_dev = plan.assemble(var, dstore, symmetric=sym)
+        assert got_dev.is_cuda and got_dev.cpu().numpy().tobytes() == want.tobytes()
+        vals = torch.full((plan.nnz,), float("nan"), dtype=dstore.dtype, device="cuda")
+        plan.assemble_async(var, dstore, vals, torch.cuda.current_stream().cuda_stream, symmetric=sym)
+        torch.cuda.synchronize()
+        assert vals.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_assembly_nonsymmetric_element_matrices(restatement, prec):
+    # a non-symmetric K (reference layout, P1 pattern kept): rows != columns
+    dim = 3
+    k = restatement.build_k("laplacian", dim).copy()
+    k[(1 + 2 * 4) * 9 + 0 * 3 + 1] *= 1.5  # block (i=1, j=2), (mu=0, nu=1)
+    v, c = fb.structured_mesh(dim, 3, 0.15, 42)
+    nv = v.size // dim
+    var = fb.make_variant("laplacian", dim, prec, "strict", element_batch_size=8, k=k)
+    assert var.path == 1
+    store = fb.integrate_mesh(var, v, c)
+    plan = fb.AssemblyPlan("laplacian", dim, c, nv)
+    rp, ci = plan.pattern()
+    want = restatement.assemble("laplacian", dim, c, nv, prec, store, rp, ci)
+    assert plan.assemble(var, store).tobytes() == want.tobytes()
 
 
 def test_assembly_shuffled_cells_and_unreferenced_vertices(restatement):
@@ -56,7 +77,14 @@ def test_assembly_shuffled_cells_and_unreferenced_vertices(restatement):
         plan = fb.AssemblyPlan("elasticity", 3, cells, nv)
         rp, ci = plan.pattern()
         want = restatement.assemble("elasticity", 3, cells, nv, "f32", store, rp, ci)
-        assert plan.assemble(var, store).tobytes() == want.tobytes()
+        assert plan.assemble(var, store, symmetric=True).tobytes() == want.tobytes()
+
+
+def _raise(plan, var, store):  # fb_assemble with an unknown flag bit
+    err = _lib.fb_error()
+    rc = plan._lib.fb_assemble(plan._h, var.handle, store.ctypes.data, store.size,
+                               np.empty(plan.nnz).ctypes.data, plan.nnz, 6, 0, C.byref(err))
+    _lib.raise_for(rc, err)
 
 
 def test_assembly_validation():
@@ -74,6 +102,8 @@ def test_assembly_validation():
     with pytest.raises(_lib.InvalidArgument, match="operator shape"):
         plan.assemble(fb.make_variant("elasticity", 2, "f64", element_batch_size=1),
                       np.zeros(c.size // 3 * 36))
+    with pytest.raises(_lib.InvalidArgument, match="flags"):
+        _raise(plan, var, store)
     with pytest.raises(_lib.InvalidArgument, match="dimension"):
         plan.assemble(fb.make_variant("laplacian", 3, "f64", element_batch_size=1), np.zeros(10 ** 4))
     del torch
@@ -90,7 +120,7 @@ def test_assembly_properties_at_size(op, dim, ne, prec):
     var = fb.make_variant(op, dim, prec, "strict")
     store = fb.integrate_mesh(var, dv, dc)
     plan = fb.AssemblyPlan(op, dim, c, nv)
-    vals = plan.assemble(var, store)
+    vals = plan.assemble(var, store, symmetric=True)
     rp, ci = plan.pattern()
     rows = torch.repeat_interleave(torch.arange(plan.rows, device="cuda"), torch.from_numpy(np.diff(rp)).cuda())
     cols = torch.from_numpy(ci).cuda().long()

@@ -60,13 +60,13 @@ def main():
             fb.status_check(st, sid)
             vals = torch.empty(plan.nnz, device="cuda", dtype=store.dtype)
             for _ in range(3):
-                plan.assemble_async(var, store, vals, sid)
+                plan.assemble_async(var, store, vals, sid, symmetric=True)
             ms = []
             for _ in range(a.steps):
                 scrub.sum(dtype=torch.int64)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                plan.assemble_async(var, store, vals, sid)
+                plan.assemble_async(var, store, vals, sid, symmetric=True)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 ms.append(e0.elapsed_time(e1))
