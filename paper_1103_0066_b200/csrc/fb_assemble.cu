@@ -31,7 +31,10 @@ namespace {
 constexpr int kAsmWarps = 4;
 constexpr int kAsmThreads = 32 * kAsmWarps;
 constexpr int kAsmSlots = 32;  // neighbours held in shared memory per thread
-constexpr int kAsmUnroll = 4;
+#ifndef FB_ASM_U
+#define FB_ASM_U 8
+#endif
+constexpr int kAsmUnroll = FB_ASM_U;  // incidences in flight per lane
 constexpr uint32_t kPad = 0xffffffffu;
 
 template <class S>
