@@ -15,6 +15,8 @@ value  = whole-job paper-count GFLOP/s (reference flop_count), device time from
 e2e    = the same metric through the public C ABI (fb_integrate_mesh) with
          pinned HOST buffers: H2D of coordinates + connectivity, kernel, D2H of
          the full element-matrix store, every step.
+assembly = global CSR assembly of the timed store on the
+         device: kernel time from CUDA events, its own HBM roofline.
 --impl reference: the unmodified reference CPU engine (oracle/_ref, built from
          /root/reference) on this host's cores, rank 0 only.
 """
@@ -58,6 +60,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-assembly", action="store_true", help="skip the global CSR assembly leg")
     return p.parse_args()
 
 
@@ -299,7 +302,7 @@ def main():
         n0 = fb.launch_counter()
         clocks.mark()
         for i in range(k):
-            scrub.sum(dtype=torch.int64)  # flush L2 with clean lines (outside the events)
+            scrub.view(torch.int64).sum()  # flush L2 with clean lines (outside the events)
             starts[i].record(stream)
             fb.integrate_mesh_async(variant, dv, dc, output, status, sid)
             ends[i].record(stream)
@@ -347,6 +350,31 @@ def main():
         ms2 = max_over_ranks(ms2)
         launches += l2
 
+        # global CSR assembly of the timed store (device-resident)
+        asm = None
+        if not args.no_assembly:
+            plan = fb.AssemblyPlan(op, dim, cells, v.size // dim)
+            vals = torch.empty(plan.nnz, dtype=tdt, device=dev)
+            for _ in range(max(args.warmup, 1)):
+                plan.assemble_async(var, out, vals, sid, symmetric=var.path in (0, 3))
+            torch.cuda.synchronize()
+            barrier()
+            a_ms = []
+            na0 = fb.launch_counter()
+            clocks.mark()
+            for _ in range(args.steps):
+                scrub.view(torch.int64).sum()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                plan.assemble_async(var, out, vals, sid, symmetric=var.path in (0, 3))
+                e1.record(stream)
+                torch.cuda.synchronize()
+                a_ms.append(e0.elapsed_time(e1))
+            clocks.unmark()
+            barrier()
+            asm = {"ms": max_over_ranks(statistics.mean(a_ms)), "nnz": plan.nnz,
+                   "launches": fb.launch_counter() - na0}
+
     # parity spot check of the timed output (full bitwise check lives in tests/)
     torch.cuda.synchronize()
 
@@ -390,6 +418,18 @@ def main():
         "ms_min": ms_min,
         "clocks": clocks.summary(),
     }
+    if asm is not None:
+        s_ = 4 if prec == "f32" else 8
+        nb_ = dim + 1
+        nv_all = v.size // dim
+        a_bytes = ne_per * nb_ * (4 + nb_) + 2 * 8 * (nv_all + 1) + ne_per * kr * kr * s_ + asm["nnz"] * s_
+        a_ach = a_bytes / (asm["ms"] * 1e-3) * 1e-9
+        line["assembly"] = {
+            "kernel": "fb_assemble_kernel (deterministic CSR gather, SURVEY 8f F3)", "ms_per_step": asm["ms"],
+            "nnz_per_gpu": asm["nnz"], "Gnnz_per_s": asm["nnz"] * world / (asm["ms"] * 1e-3) * 1e-9,
+            "roofline": {"bound": "hbm", "achieved": a_ach, "peak": peak, "unit": "GB/s", "frac": a_ach / peak,
+                         "algorithmic_bytes_per_launch": a_bytes},
+            "gpu_launches": asm["launches"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(op, dim, prec, v, cells)
     if rank == 0:

@@ -63,7 +63,7 @@ def main():
                 plan.assemble_async(var, store, vals, sid, symmetric=True)
             ms = []
             for _ in range(a.steps):
-                scrub.sum(dtype=torch.int64)
+                scrub.view(torch.int64).sum()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 plan.assemble_async(var, store, vals, sid, symmetric=True)

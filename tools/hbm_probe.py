@@ -28,12 +28,12 @@ def main():
     out = {}
     for mb in (160, 1024, 4096):
         n = mb << 20
-        a = torch.empty(n, dtype=torch.uint8, device="cuda")
-        b = torch.empty(n, dtype=torch.uint8, device="cuda")
-        a.fill_(1)
-        t = timed(lambda: b.fill_(3))
+        a = torch.empty(n // 4, dtype=torch.float32, device="cuda")
+        b = torch.empty(n // 4, dtype=torch.float32, device="cuda")
+        a.fill_(1.0)
+        t = timed(lambda: b.fill_(3.0))
         out[f"write_{mb}MB_GBs"] = n / t * 1e-9
-        t = timed(lambda: a.view(torch.int32).sum(dtype=torch.int64))
+        t = timed(lambda: a.sum())
         out[f"read_{mb}MB_GBs"] = n / t * 1e-9
         t = timed(lambda: b.copy_(a))
         out[f"copy_{mb}MB_GBs"] = 2 * n / t * 1e-9

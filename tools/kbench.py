@@ -53,7 +53,7 @@ def main():
                         fb.integrate_mesh_async(var, dv, dc, out, st, sid)
                     ms = []
                     for _ in range(a.steps):
-                        scrub.sum(dtype=torch.int64)
+                        scrub.view(torch.int64).sum()
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record()
                         fb.integrate_mesh_async(var, dv, dc, out, st, sid)

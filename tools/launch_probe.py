@@ -47,7 +47,7 @@ def main():
         def single(n=20):
             t = []
             for _ in range(n):
-                scrub.sum(dtype=torch.int64)
+                scrub.view(torch.int64).sum()
                 a, b = ev(), ev()
                 a.record(s)
                 fb.integrate_mesh_async(var, dv, dc, out, st, sid)
@@ -62,7 +62,7 @@ def main():
             fb.integrate_mesh_async(var, dv, dc, out, st, s.cuda_stream)
         t = []
         for _ in range(20):
-            scrub.sum(dtype=torch.int64)
+            scrub.view(torch.int64).sum()
             a, b = ev(), ev()
             a.record(s)
             g.replay()
@@ -70,7 +70,7 @@ def main():
             torch.cuda.synchronize()
             t.append(a.elapsed_time(b) * 1e3)
         res["graph_us"] = statistics.median(t)
-        scrub.sum(dtype=torch.int64)
+        scrub.view(torch.int64).sum()
         a, b = ev(), ev()
         a.record(s)
         for _ in range(20):
@@ -80,7 +80,7 @@ def main():
         res["b2b_per_launch_us"] = a.elapsed_time(b) * 1e3 / 20
         t = []
         for _ in range(20):
-            scrub.sum(dtype=torch.int64)
+            scrub.view(torch.int64).sum()
             a, b = ev(), ev()
             a.record(s)
             b.record(s)
