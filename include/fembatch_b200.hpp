@@ -27,6 +27,7 @@
 #include <vector>
 
 struct fb_variant;
+struct fb_assembly;
 
 namespace fembatch {
 
@@ -192,5 +193,30 @@ std::vector<double> unpack_element_matrix(const ElementMatrixStore& store, const
                                           const FormSpec& spec, std::int64_t element);
 void write_store(std::ostream& os, const ElementMatrixStore& store);
 ElementMatrixStore read_store(std::istream& is);
+
+// ---- global assembly (GPU extension; SURVEY 8f row F3 -- the reference's
+// declared non-goal).  dof(v, c) = v*nc + c, nc = dim for
+// elasticity else 1; values = the serial element-order sum, bitwise.
+struct CsrMatrix {
+  std::int64_t rows = 0;
+  std::vector<std::int64_t> row_ptr;
+  std::vector<std::int32_t> col_idx;
+  Precision precision = Precision::f64;
+  ScalarArray values;
+};
+
+struct AssemblyPlan {
+  Operator op = Operator::laplacian;
+  int dim = 0;
+  std::int64_t rows = 0, nnz = 0;
+  std::shared_ptr<fb_assembly> device;  // pattern + incidence lists (host built, uploaded per device)
+};
+
+AssemblyPlan make_assembly_plan(Operator op, const Mesh& mesh);
+// `store` must hold the element matrices of the plan's mesh (e.g. from
+// integrate_mesh); `symmetric` = every element matrix is bitwise symmetric
+// (true for integrate_mesh output of the reference forms), read as columns.
+CsrMatrix assemble_global(const KernelVariant& variant, const AssemblyPlan& plan, const ElementMatrixStore& store,
+                          bool symmetric = false, int device = 0);
 
 }  // namespace fembatch

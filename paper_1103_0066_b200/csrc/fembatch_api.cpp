@@ -557,4 +557,44 @@ ElementMatrixStore read_store(std::istream& is)
   return s;
 }
 
+// ---- global assembly ------------------------------------------------------
+AssemblyPlan make_assembly_plan(Operator op, const Mesh& mesh)
+{
+  fb_error err{};
+  fb_assembly* a = fb_assembly_create(static_cast<int>(op), mesh.dim, mesh.cells.data(), mesh.num_elements(),
+                                      mesh.num_vertices(), &err);
+  if (!a)
+    check(err.code ? err.code : FB_ERR_INVALID_ARGUMENT, err);
+  AssemblyPlan p;
+  p.op = op;
+  p.dim = mesh.dim;
+  p.device = std::shared_ptr<fb_assembly>(a, fb_assembly_free);
+  p.rows = fb_assembly_rows(a);
+  p.nnz = fb_assembly_nnz(a);
+  return p;
+}
+
+CsrMatrix assemble_global(const KernelVariant& v, const AssemblyPlan& plan, const ElementMatrixStore& store,
+                          bool symmetric, int device)
+{
+  if (!v.device || !plan.device)
+    throw std::invalid_argument("variant or assembly plan was not created for the GPU");
+  if (store.precision != v.config.precision || store.dim != plan.dim)
+    throw std::invalid_argument("store does not match variant / plan");
+  CsrMatrix m;
+  m.rows = plan.rows;
+  m.precision = store.precision;
+  m.row_ptr.resize(plan.rows + 1);
+  m.col_idx.resize(plan.nnz);
+  fb_error err{};
+  check(fb_assembly_pattern(plan.device.get(), m.row_ptr.data(), plan.rows + 1, m.col_idx.data(), plan.nnz, &err),
+        err);
+  m.values = make_scalar_array(store.precision, plan.nnz);
+  check(fb_assemble(plan.device.get(), v.device.get(), data_ptr(store.data),
+                    scalar_array_size(store.data), data_ptr(m.values), plan.nnz,
+                    symmetric ? FB_ASSEMBLE_SYMMETRIC : 0, device, &err),
+        err);
+  return m;
+}
+
 }  // namespace fembatch

@@ -372,6 +372,65 @@ TEST_CASE(store_round_trip, true)
   CHECK_THROWS_AS(read_store(junk), std::runtime_error);
 }
 
+TEST_CASE(assembly_plan_pattern_and_validation, false)
+{
+  const Mesh mesh = structured_simplicial_mesh(2, 2);  // 9 vertices, 8 triangles
+  const AssemblyPlan lap = make_assembly_plan(Operator::laplacian, mesh);
+  CHECK(lap.rows == 9);
+  const AssemblyPlan el = make_assembly_plan(Operator::elasticity, mesh);
+  CHECK(el.rows == 18 && el.nnz == 4 * lap.nnz);
+  Mesh bad = mesh;
+  bad.cells[4] = 99;  // cell 1
+  CHECK_THROWS_WITH_AS(make_assembly_plan(Operator::laplacian, bad), "out of range in cell 1", std::invalid_argument);
+  bad = mesh;
+  bad.cells[5] = bad.cells[3];  // cell 1 repeats a vertex
+  CHECK_THROWS_WITH_AS(make_assembly_plan(Operator::laplacian, bad), "repeated vertex in cell 1",
+                       std::invalid_argument);
+}
+
+TEST_CASE(global_assembly_is_the_serial_element_sum, true)
+{
+  const Mesh mesh = jitter_mesh(structured_simplicial_mesh(3, 3), 0.15, 42);
+  for (Precision p : {Precision::f64, Precision::f32})
+    for (Operator op : {Operator::laplacian, Operator::elasticity})
+    {
+      const KernelConfig c = config_of(16, 1, false, false, p);
+      const ElementMatrixStore s = integrate(op, mesh, c);
+      const FormSpec spec = make_form_spec(op, 3);
+      const KernelVariant v = specialize_kernel(spec, build_analytic_tensor(op, 3), c);
+      const AssemblyPlan plan = make_assembly_plan(op, mesh);
+      const CsrMatrix a = assemble_global(v, plan, s, true);
+      const CsrMatrix b = assemble_global(v, plan, s, false);
+      CHECK(a.rows == plan.rows && static_cast<std::int64_t>(a.col_idx.size()) == plan.nnz);
+      // serial element-order sum in engine precision (the definition)
+      const int nc = op == Operator::elasticity ? 3 : 1, kr = spec.krows();
+      std::vector<double> want(plan.nnz, 0.0);
+      std::vector<float> want32(plan.nnz, 0.0f);
+      for (std::int64_t e = 0; e < mesh.num_elements(); ++e)
+        for (int j = 0; j < kr; ++j)
+          for (int i = 0; i < kr; ++i)
+          {
+            const std::int64_t row = std::int64_t(mesh.cells[e * 4 + i % 4]) * nc + i / 4;
+            const std::int32_t col = mesh.cells[e * 4 + j % 4] * nc + j / 4;
+            std::int64_t z = a.row_ptr[row];
+            while (a.col_idx[z] != col)
+              ++z;
+            const double x = scalar_array_at(s.data, e * kr * kr + i + std::int64_t(j) * kr);
+            if (p == Precision::f64)
+              want[z] = want[z] + x;
+            else
+              want32[z] = want32[z] + static_cast<float>(x);
+          }
+      bool same = true;
+      for (std::int64_t z = 0; same && z < plan.nnz; ++z)
+      {
+        const double w = p == Precision::f64 ? want[z] : double(want32[z]);
+        same = scalar_array_at(a.values, z) == w && scalar_array_at(b.values, z) == w;
+      }
+      CHECK(same);
+    }
+}
+
 }  // namespace
 
 int main(int argc, char** argv)
