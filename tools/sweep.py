@@ -88,7 +88,7 @@ def main():
                         for d in range(G):
                             with torch.cuda.device(d):
                                 sid = torch.cuda.current_stream().cuda_stream
-                                scrubs[d].sum(dtype=torch.int64)
+                                scrubs[d].view(torch.int64).sum()
                                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                                 vs, cs, out, st = shards[d]
                                 if it == 0:
