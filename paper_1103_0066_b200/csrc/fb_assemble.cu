@@ -2,18 +2,18 @@
 // (the reference stops at element matrices).
 //
 // Deterministic gather, no atomics.  A warp owns 32 consecutive vertices and
-// one component pair (ci, cj); lane l walks vertex v = 32g + l's incident
-// elements in ascending element order (sliced SELL-32 lists: every lane
-// load of the plan is coalesced) and adds row a (v's local index),
-// component block (ci, cj), of each element matrix into per-neighbour
+// one row component ci; lane l walks vertex v = 32g + l's incident elements
+// in ascending element order (sliced SELL-32 lists: every lane load of the
+// plan is coalesced) and adds row a + ci*nb (v's local row) of each element
+// matrix, all column components, into per-(neighbour, component)
 // accumulators in shared memory ([slot][thread], conflict-free).  Every CSR
 // entry thus receives its contributions in ascending element order from +0
 // -- bitwise the serial element loop of the oracle (oracle/fb_oracle.c
 // fbo_assemble).  When the variant's element matrices are bitwise symmetric
 // (the sparse-symmetric kernel paths mirror one triangle) the row is read as
-// the contiguous column (one 16-byte load in 3D f32).  Incidences are
+// the contiguous column with the widest aligned vector loads.  Incidences are
 // processed U at a time so a lane has U element rows in flight.  Vertices
-// with more than kAsmSlots neighbours accumulate directly in their own
+// with more neighbours than fit (AsmShape::SLOTS) accumulate directly in their own
 // (thread-private) rows of the output.
 #include <atomic>
 #include <cstdint>
@@ -28,13 +28,20 @@ std::atomic<long long>& launch_counter();
 
 namespace {
 
-constexpr int kAsmWarps = 4;
-constexpr int kAsmThreads = 32 * kAsmWarps;
-constexpr int kAsmSlots = 32;  // neighbours held in shared memory per thread
 #ifndef FB_ASM_U
 #define FB_ASM_U 8
 #endif
-constexpr int kAsmUnroll = FB_ASM_U;  // incidences in flight per lane
+// CTA shape: a thread keeps SLOTS neighbours x nc components in shared
+// memory (<= 48 KB static per CTA); vertices with more neighbours accumulate
+// in their own rows of the output.
+template <class S, int NC>
+struct AsmShape {
+  static constexpr int WARPS = NC == 1 ? 4 : 2;
+  static constexpr int SLOTS = NC == 1 ? 32 : 24;
+  // incidences in flight per lane (each holds a krows-scalar element row)
+  static constexpr int U = NC == 1 ? FB_ASM_U : (NC == 2 || sizeof(S) == 4 ? 4 : 2);
+  static_assert(SLOTS * NC * 32 * WARPS * sizeof(S) <= 48 * 1024, "static smem");
+};
 constexpr uint32_t kPad = 0xffffffffu;
 
 template <class S>
@@ -44,76 +51,96 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 template <>
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
-// The NB entries of element-matrix row i = aa + ci*NB, columns b + cj*NB.
-template <class S, int NB, int KROWS, bool SYM>
-__device__ __forceinline__ void load_row(const S* blk, int i, int cj, S (&r)[NB])
+// N contiguous scalars from p, whose address is a multiple of A bytes
+// (A = 16, 8 or 4): the widest aligned vector loads.
+template <class S, int N, int A>
+__device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
+{
+  constexpr int W = A / static_cast<int>(sizeof(S)) > 0 ? A / static_cast<int>(sizeof(S)) : 1;  // scalars per load
+  static_assert(N % W == 0, "vector width must divide the run");
+#pragma unroll
+  for (int t = 0; t < N; t += W)
+  {
+    if constexpr (W == 4)
+    {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p + t));
+      r[t] = q.x;
+      r[t + 1] = q.y;
+      r[t + 2] = q.z;
+      r[t + 3] = q.w;
+    }
+    else if constexpr (W == 2 && sizeof(S) == 8)
+    {
+      const double2 q = __ldg(reinterpret_cast<const double2*>(p + t));
+      r[t] = q.x;
+      r[t + 1] = q.y;
+    }
+    else if constexpr (W == 2)
+    {
+      const float2 q = __ldg(reinterpret_cast<const float2*>(p + t));
+      r[t] = q.x;
+      r[t + 1] = q.y;
+    }
+    else
+      r[t] = __ldg(p + t);
+  }
+}
+
+__host__ __device__ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
+
+// Row i = aa + ci*NB of an element matrix, all KROWS columns (j = b + cj*NB).
+// SYM: A(i, j) == A(j, i), so the row is read as the contiguous column i.
+template <class S, int KROWS, bool SYM>
+__device__ __forceinline__ void load_row(const S* blk, int i, S (&r)[KROWS])
 {
   if constexpr (SYM)
   {
-    // A(i, j) == A(j, i): the contiguous column i, rows cj*NB .. cj*NB+NB-1
-    const S* p = blk + cj * NB + i * KROWS;
-    if constexpr (NB == 4 && sizeof(S) == 4)
-    {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(p));
-      r[0] = q.x;
-      r[1] = q.y;
-      r[2] = q.z;
-      r[NB - 1] = q.w;
-    }
-    else if constexpr (NB == 4 && sizeof(S) == 8)
-    {
-      const double2 q0 = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 q1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
-      r[0] = q0.x;
-      r[1] = q0.y;
-      r[2] = q1.x;
-      r[NB - 1] = q1.y;
-    }
-    else
-    {
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-        r[b] = __ldg(p + b);
-    }
+    // the store is 16-byte aligned (host check) and krows^2*s is a multiple
+    // of this alignment, so column i starts on an A-byte boundary
+    constexpr int A = gcd_i(KROWS * static_cast<int>(sizeof(S)), 16);
+    load_vec<S, KROWS, A>(blk + i * KROWS, r);
   }
   else
   {
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-      r[b] = __ldg(blk + i + (b + cj * NB) * KROWS);
+    for (int j = 0; j < KROWS; ++j)
+      r[j] = __ldg(blk + i + j * KROWS);
   }
 }
 
+// A warp owns 32 consecutive vertices and one component ci: lane l = vertex
+// v = 32g + l, rows (v, ci), all nc column components per neighbour.
 template <class S, int DIM, int NC, bool SYM>
-__global__ void __launch_bounds__(kAsmThreads) fb_assemble_kernel(const AsmArgs a)
+__global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kernel(const AsmArgs a)
 {
-  constexpr int NB = DIM + 1, KROWS = NB * NC, NK = KROWS * KROWS, NC2 = NC * NC;
-  constexpr int U = kAsmUnroll;
-  __shared__ S acc_s[kAsmSlots * kAsmThreads];
+  constexpr int NB = DIM + 1, KROWS = NB * NC, NK = KROWS * KROWS;
+  constexpr int T = 32 * AsmShape<S, NC>::WARPS;
+  constexpr int SLOTS = AsmShape<S, NC>::SLOTS;  // neighbours held in shared memory
+  constexpr int U = AsmShape<S, NC>::U;
+  __shared__ S acc_s[SLOTS * NC * T];
   S* acc = acc_s + threadIdx.x;
   S* vals = static_cast<S*>(a.values);
   const S* store = static_cast<const S*>(a.store);
   const int lane = threadIdx.x & 31;
   const int64_t ngroups = (a.nv + 31) / 32;
-  const int64_t nwarps = ngroups * NC2;
-  for (int64_t w = static_cast<int64_t>(blockIdx.x) * kAsmWarps + (threadIdx.x >> 5); w < nwarps;
-       w += static_cast<int64_t>(gridDim.x) * kAsmWarps)
+  const int64_t nwarps = ngroups * NC;
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); w < nwarps;
+       w += static_cast<int64_t>(gridDim.x) * (T / 32))
   {
-    const int64_t g = w / NC2;
-    const int cp = static_cast<int>(w - g * NC2);
-    const int ci = cp / NC, cj = cp % NC;
+    const int64_t g = w / NC;
+    const int ci = static_cast<int>(w - g * NC);
     const int64_t v = g * 32 + lane;
     const bool live = v < a.nv;
     const int64_t r0 = live ? __ldg(a.nbr_ptr + v) : 0;
     const int deg = live ? static_cast<int>(__ldg(a.nbr_ptr + v + 1) - r0) : 0;
-    const int64_t row = r0 * NC2 + static_cast<int64_t>(ci) * deg * NC + cj;  // + k*NC
-    const bool in_smem = deg <= kAsmSlots;
+    const int64_t row = r0 * NC * NC + static_cast<int64_t>(ci) * deg * NC;  // + k*NC + cj
+    const bool in_smem = deg <= SLOTS;
     if (in_smem)
-      for (int k = 0; k < deg; ++k)
-        acc[k * kAsmThreads] = S(0);
+      for (int k = 0; k < deg * NC; ++k)
+        acc[k * T] = S(0);
     else
-      for (int k = 0; k < deg; ++k)
-        vals[row + static_cast<int64_t>(k) * NC] = S(0);
+      for (int k = 0; k < deg * NC; ++k)
+        vals[row + k] = S(0);
     const int64_t q0 = __ldg(a.goff + g), q1 = __ldg(a.goff + g + 1);
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
@@ -125,14 +152,14 @@ __global__ void __launch_bounds__(kAsmThreads) fb_assemble_kernel(const AsmArgs 
         pk[u] = qu < q1 ? __ldg(a.spk + qu) : kPad;
         ps[u] = qu < q1 ? __ldg(a.spos + qu) : 0u;
       }
-      S r[U][NB];
+      S r[U][KROWS];
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (pk[u] != kPad)
         {
           const int64_t e = pk[u] >> 2;
           const int aa = static_cast<int>(pk[u] & 3u);
-          load_row<S, NB, KROWS, SYM>(store + e * NK, aa + ci * NB, cj, r[u]);
+          load_row<S, KROWS, SYM>(store + e * NK, aa + ci * NB, r[u]);
         }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -142,40 +169,45 @@ __global__ void __launch_bounds__(kAsmThreads) fb_assemble_kernel(const AsmArgs 
           for (int b = 0; b < NB; ++b)
           {
             const int k = (ps[u] >> (8 * b)) & 0xffu;
-            if (in_smem)
-              acc[k * kAsmThreads] = add_rn(acc[k * kAsmThreads], r[u][b]);
-            else
+#pragma unroll
+            for (int cj = 0; cj < NC; ++cj)
             {
-              S* p = vals + row + static_cast<int64_t>(k) * NC;
-              *p = add_rn(*p, r[u][b]);
+              if (in_smem)
+                acc[(k * NC + cj) * T] = add_rn(acc[(k * NC + cj) * T], r[u][b + cj * NB]);
+              else
+              {
+                S* p = vals + row + k * NC + cj;
+                *p = add_rn(*p, r[u][b + cj * NB]);
+              }
             }
           }
         }
     }
     if (in_smem)
-      for (int k = 0; k < deg; ++k)
-        vals[row + static_cast<int64_t>(k) * NC] = acc[k * kAsmThreads];
+      for (int k = 0; k < deg * NC; ++k)
+        vals[row + k] = acc[k * T];
   }
 }
 
 template <class S, int DIM, int NC, bool SYM>
 cudaError_t go(const AsmArgs& a, cudaStream_t st)
 {
-  const int64_t nwarps = (a.nv + 31) / 32 * NC * NC;
+  constexpr int T = 32 * AsmShape<S, NC>::WARPS;
+  const int64_t nwarps = (a.nv + 31) / 32 * NC;
   if (nwarps <= 0)
     return cudaSuccess;
   static int grid_cap = 0;
   if (grid_cap == 0)
   {
     int blocks = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_kernel<S, DIM, NC, SYM>, kAsmThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_kernel<S, DIM, NC, SYM>, T, 0);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid_cap = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
   }
-  const int64_t need = (nwarps + kAsmWarps - 1) / kAsmWarps;
+  const int64_t need = (nwarps + T / 32 - 1) / (T / 32);
   const unsigned grid = static_cast<unsigned>(need < grid_cap ? need : grid_cap);
-  fb_assemble_kernel<S, DIM, NC, SYM><<<grid, kAsmThreads, 0, st>>>(a);
+  fb_assemble_kernel<S, DIM, NC, SYM><<<grid, T, 0, st>>>(a);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
