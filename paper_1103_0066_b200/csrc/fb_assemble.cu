@@ -31,16 +31,24 @@ namespace {
 #ifndef FB_ASM_U
 #define FB_ASM_U 8
 #endif
-// CTA shape: a thread keeps SLOTS neighbours x nc components in shared
-// memory (<= 48 KB static per CTA); vertices with more neighbours accumulate
-// in their own rows of the output.
+// Work split and CTA shape.  A warp owns 32 consecutive vertices, one row
+// component ci and NCW of the nc column components (NCW = 1: one (ci, cj)
+// block per warp, more warps in flight; NCW = nc: the whole element row per
+// load, fewer plan re-reads) -- chosen per shape by measurement
+// (tools/asmbench.py A/B).  A thread keeps SLOTS neighbours x NCW components
+// in shared memory (<= 48 KB static per CTA); vertices with more neighbours
+// accumulate in their own rows of the output.  U = incidences in flight per
+// lane.
 template <class S, int NC>
 struct AsmShape {
-  static constexpr int WARPS = NC == 1 ? 4 : 2;
-  static constexpr int SLOTS = NC == 1 ? 32 : 24;
-  // incidences in flight per lane (each holds a krows-scalar element row)
-  static constexpr int U = NC == 1 ? FB_ASM_U : (NC == 2 || sizeof(S) == 4 ? 4 : 2);
-  static_assert(SLOTS * NC * 32 * WARPS * sizeof(S) <= 48 * 1024, "static smem");
+  static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : 1;
+  static constexpr int WARPS = NCW == 1 ? 4 : 2;
+  static constexpr int SLOTS = NCW == 1 ? 32 : 24;
+  static constexpr int U = NCW == 1 ? FB_ASM_U : 4;
+  // batch the slot updates of one incidence (all loads, adds, stores): faster
+  // in FP32, slower in FP64 (register pressure) -- A/B measured
+  static constexpr bool BATCH = sizeof(S) == 4;
+  static_assert(SLOTS * NCW * 32 * WARPS * sizeof(S) <= 48 * 1024, "static smem");
 };
 constexpr uint32_t kPad = 0xffffffffu;
 
@@ -88,59 +96,63 @@ __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
 
 __host__ __device__ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
 
-// Row i = aa + ci*NB of an element matrix, all KROWS columns (j = b + cj*NB).
-// SYM: A(i, j) == A(j, i), so the row is read as the contiguous column i.
-template <class S, int KROWS, bool SYM>
-__device__ __forceinline__ void load_row(const S* blk, int i, S (&r)[KROWS])
+// Row i = aa + ci*NB of an element matrix, columns j = b + cj*NB for the
+// N = NB*NCW columns of components cj0 .. cj0+NCW-1 (a contiguous run).
+// SYM: A(i, j) == A(j, i), so the run is read from column i, contiguous.
+template <class S, int NB, int KROWS, int N, bool SYM>
+__device__ __forceinline__ void load_row(const S* blk, int i, int cj0, S (&r)[N])
 {
   if constexpr (SYM)
   {
-    // the store is 16-byte aligned (host check) and krows^2*s is a multiple
-    // of this alignment, so column i starts on an A-byte boundary
-    constexpr int A = gcd_i(KROWS * static_cast<int>(sizeof(S)), 16);
-    load_vec<S, KROWS, A>(blk + i * KROWS, r);
+    // the store is 16-byte aligned (host check); krows^2*s, krows*s and
+    // nb*s are multiples of A, so the run starts on an A-byte boundary
+    constexpr int A = gcd_i(gcd_i(KROWS * static_cast<int>(sizeof(S)), NB * static_cast<int>(sizeof(S))), 16);
+    load_vec<S, N, A>(blk + i * KROWS + cj0 * NB, r);
   }
   else
   {
 #pragma unroll
-    for (int j = 0; j < KROWS; ++j)
-      r[j] = __ldg(blk + i + j * KROWS);
+    for (int j = 0; j < N; ++j)
+      r[j] = __ldg(blk + i + (cj0 * NB + j) * KROWS);
   }
 }
 
-// A warp owns 32 consecutive vertices and one component ci: lane l = vertex
-// v = 32g + l, rows (v, ci), all nc column components per neighbour.
 template <class S, int DIM, int NC, bool SYM>
 __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kernel(const AsmArgs a)
 {
+  using Sh = AsmShape<S, NC>;
   constexpr int NB = DIM + 1, KROWS = NB * NC, NK = KROWS * KROWS;
-  constexpr int T = 32 * AsmShape<S, NC>::WARPS;
-  constexpr int SLOTS = AsmShape<S, NC>::SLOTS;  // neighbours held in shared memory
-  constexpr int U = AsmShape<S, NC>::U;
-  __shared__ S acc_s[SLOTS * NC * T];
+  constexpr int NCW = Sh::NCW, NWC = NC / NCW;  // column components per warp, warps per row
+  constexpr int T = 32 * Sh::WARPS;
+  constexpr int SLOTS = Sh::SLOTS;
+  constexpr int U = Sh::U;
+  __shared__ S acc_s[SLOTS * NCW * T];
   S* acc = acc_s + threadIdx.x;
   S* vals = static_cast<S*>(a.values);
   const S* store = static_cast<const S*>(a.store);
   const int lane = threadIdx.x & 31;
   const int64_t ngroups = (a.nv + 31) / 32;
-  const int64_t nwarps = ngroups * NC;
+  const int64_t nwarps = ngroups * NC * NWC;
   for (int64_t w = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); w < nwarps;
        w += static_cast<int64_t>(gridDim.x) * (T / 32))
   {
-    const int64_t g = w / NC;
-    const int ci = static_cast<int>(w - g * NC);
+    const int64_t g = w / (NC * NWC);
+    const int sub = static_cast<int>(w - g * (NC * NWC));
+    const int ci = sub / NWC, cj0 = (sub % NWC) * NCW;
     const int64_t v = g * 32 + lane;
     const bool live = v < a.nv;
     const int64_t r0 = live ? __ldg(a.nbr_ptr + v) : 0;
     const int deg = live ? static_cast<int>(__ldg(a.nbr_ptr + v + 1) - r0) : 0;
-    const int64_t row = r0 * NC * NC + static_cast<int64_t>(ci) * deg * NC;  // + k*NC + cj
+    // value (neighbour slot k, column component cj0 + c) at row + k*NC + c
+    const int64_t row = r0 * NC * NC + static_cast<int64_t>(ci) * deg * NC + cj0;
     const bool in_smem = deg <= SLOTS;
     if (in_smem)
-      for (int k = 0; k < deg * NC; ++k)
+      for (int k = 0; k < deg * NCW; ++k)
         acc[k * T] = S(0);
     else
-      for (int k = 0; k < deg * NC; ++k)
-        vals[row + k] = S(0);
+      for (int k = 0; k < deg; ++k)
+        for (int c = 0; c < NCW; ++c)
+          vals[row + k * NC + c] = S(0);
     const int64_t q0 = __ldg(a.goff + g), q1 = __ldg(a.goff + g + 1);
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
@@ -152,40 +164,61 @@ __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kerne
         pk[u] = qu < q1 ? __ldg(a.spk + qu) : kPad;
         ps[u] = qu < q1 ? __ldg(a.spos + qu) : 0u;
       }
-      S r[U][KROWS];
+      S r[U][NB * NCW];
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (pk[u] != kPad)
         {
           const int64_t e = pk[u] >> 2;
           const int aa = static_cast<int>(pk[u] & 3u);
-          load_row<S, KROWS, SYM>(store + e * NK, aa + ci * NB, r[u]);
+          load_row<S, NB, KROWS, NB * NCW, SYM>(store + e * NK, aa + ci * NB, cj0, r[u]);
         }
+      // one incidence at a time (two incidences may share a neighbour); with
+      // BATCH, the nb*NCW slots of an incidence (distinct: distinct element
+      // vertices) are all loaded, added and stored as a group
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (pk[u] != kPad)
         {
+          int at[NB * NCW];
 #pragma unroll
           for (int b = 0; b < NB; ++b)
           {
-            const int k = (ps[u] >> (8 * b)) & 0xffu;
+            const int k = static_cast<int>((ps[u] >> (8 * b)) & 0xffu);
 #pragma unroll
-            for (int cj = 0; cj < NC; ++cj)
-            {
-              if (in_smem)
-                acc[(k * NC + cj) * T] = add_rn(acc[(k * NC + cj) * T], r[u][b + cj * NB]);
-              else
-              {
-                S* p = vals + row + k * NC + cj;
-                *p = add_rn(*p, r[u][b + cj * NB]);
-              }
-            }
+            for (int c = 0; c < NCW; ++c)
+              at[b * NCW + c] = in_smem ? (k * NCW + c) * T : k * NC + c;
+          }
+          S* base = in_smem ? acc : vals + row;
+          if constexpr (Sh::BATCH)
+          {
+            S cur[NB * NCW];
+#pragma unroll
+            for (int t = 0; t < NB * NCW; ++t)
+              cur[t] = base[at[t]];
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int c = 0; c < NCW; ++c)
+                cur[b * NCW + c] = add_rn(cur[b * NCW + c], r[u][b + c * NB]);
+#pragma unroll
+            for (int t = 0; t < NB * NCW; ++t)
+              base[at[t]] = cur[t];
+          }
+          else
+          {
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int c = 0; c < NCW; ++c)
+                base[at[b * NCW + c]] = add_rn(base[at[b * NCW + c]], r[u][b + c * NB]);
           }
         }
     }
     if (in_smem)
-      for (int k = 0; k < deg * NC; ++k)
-        vals[row + k] = acc[k * T];
+      for (int k = 0; k < deg; ++k)
+        for (int c = 0; c < NCW; ++c)
+          vals[row + k * NC + c] = acc[(k * NCW + c) * T];
   }
 }
 
@@ -193,7 +226,7 @@ template <class S, int DIM, int NC, bool SYM>
 cudaError_t go(const AsmArgs& a, cudaStream_t st)
 {
   constexpr int T = 32 * AsmShape<S, NC>::WARPS;
-  const int64_t nwarps = (a.nv + 31) / 32 * NC;
+  const int64_t nwarps = (a.nv + 31) / 32 * NC * (NC / AsmShape<S, NC>::NCW);
   if (nwarps <= 0)
     return cudaSuccess;
   static int grid_cap = 0;
