@@ -322,18 +322,22 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
   const bool direct_out = j.out_dev == dev;
   const bool whole = direct_out && (j.kind == Kind::Packed ? j.g_dev == dev : j.cells_dev == dev)
                      && (j.coeffs == nullptr || j.coeff_dev == dev);
-  // Chunk so a chunk's output is ~64 MB; a fully device-resident job is one chunk.
-  int64_t chunk = s1 - s0;
-  if (!whole)
+  // Host-staged jobs run as a chunk pipeline whose outputs start at ~4 MB and
+  // double up to 64 MB: the first device->host copy starts early (PCIe D2H of
+  // the store dominates), later chunks amortise per-launch cost.  A fully
+  // device-resident job is one chunk.
+  auto slots_for = [&](int64_t bytes)
   {
-    const int64_t per = std::max<int64_t>(1, (64ll << 20) / (j.nk * static_cast<int64_t>(ss)));
-    chunk = std::max<int64_t>(fbk::kTile, per / fbk::kTile * fbk::kTile);
-  }
+    const int64_t per = std::max<int64_t>(1, bytes / (j.nk * static_cast<int64_t>(ss)));
+    return std::max<int64_t>(fbk::kTile, per / fbk::kTile * fbk::kTile);
+  };
+  int64_t chunk = whole ? s1 - s0 : slots_for(4ll << 20);
+  const int64_t chunk_max = whole ? s1 - s0 : slots_for(64ll << 20);
 
   int which = 0;
-  for (int64_t c0 = s0; c0 < s1; c0 += chunk, which ^= 1)
+  for (int64_t c0 = s0, c1 = 0; c0 < s1; c0 = c1, which ^= 1, chunk = std::min(chunk_max, 2 * chunk))
   {
-    const int64_t c1 = std::min(s1, c0 + chunk);
+    c1 = std::min(s1, c0 + chunk);
     cudaStream_t st = ctx.st[which];
     fbk::LaunchArgs a = base;
     a.slot0 = c0;
