@@ -201,6 +201,10 @@ int fb_integrate_packed_async(const fb_variant* v, int dim, const void* g,
                               int64_t num_batches, int64_t num_elements,
                               const double* coefficients, void* out,
                               int64_t out_len, void* stream, fb_error* err);
+/* GPU pack_geometry on device buffers (degenerate cells -> status). */
+int fb_pack_geometry_async(const fb_mesh_view* mesh, int element_batch_size, int precision,
+                           void* g_out, int64_t g_len, int64_t* status, void* stream,
+                           fb_error* err);
 int fb_status_reset(int64_t* status, void* stream, fb_error* err);
 /* Synchronises `stream`, then maps the status words to the reference
  * exception (FB_ERR_RUNTIME "degenerate element: det(J) <= 0 in cell N"). */

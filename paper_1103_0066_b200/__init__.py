@@ -21,6 +21,7 @@ from .engine import (  # noqa: F401
     make_form_spec,
     make_variant,
     pack_geometry,
+    pack_geometry_async,
     specialize_kernel,
     status_check,
     status_reset,

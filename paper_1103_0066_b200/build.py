@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB
     for s in CPP_SOURCES:
         obj = os.path.join(build_dir, s + ".o")
         jobs.append((obj, ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-pthread",
-                           "-I", os.path.join(CUDA_HOME, "include"), *inc,
+                           "-I", os.path.join(CUDA_HOME, "include"), *dflags, *inc,
                            "-c", os.path.join(CSRC, s), "-o", obj]))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:

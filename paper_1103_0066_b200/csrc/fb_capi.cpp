@@ -797,6 +797,47 @@ int fb_pack_geometry(const fb_mesh_view* mesh, int bs, int precision, void* g_ou
                  });
 }
 
+int fb_pack_geometry_async(const fb_mesh_view* mesh, int bs, int precision, void* g_out, int64_t g_len,
+                           int64_t* status, void* stream, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   validate_mesh_view(mesh);
+                   if (bs < 1)
+                     invalid("element_batch_size must be positive");
+                   if (precision != FB_F32 && precision != FB_F64)
+                     invalid("unknown precision");
+                   const int dd = mesh->dim * mesh->dim;
+                   const int64_t nslots = (mesh->num_elements + bs - 1) / bs * bs;
+                   if (g_len != nslots * dd)
+                     invalid("geometry buffer holds " + std::to_string(g_len) + " scalars; packing needs "
+                             + std::to_string(nslots * dd));
+                   if (!status)
+                     invalid("null status buffer");
+                   if (nslots == 0)
+                     return;
+                   fbk::LaunchArgs a{};
+                   a.vtx = mesh->vertices;
+                   a.cells = mesh->cells;
+                   a.out = g_out;
+                   a.status = reinterpret_cast<long long*>(status);
+                   a.nv = mesh->num_vertices;
+                   a.ne = mesh->num_elements;
+                   a.cells_aligned16 = aligned16(a.cells);
+                   a.vtx_aligned16 = aligned16(a.vtx);
+                   for (int64_t off = 0; off < nslots; off += kMaxLaunchSlots)
+                   {
+                     fbk::LaunchArgs c = a;
+                     c.slot0 = off;
+                     c.nloc = std::min(kMaxLaunchSlots, nslots - off);
+                     c.out = static_cast<char*>(g_out) + off * dd * scalar_size(precision);
+                     cuda_check(fbk::launch_pack(mesh->dim, precision, c, static_cast<cudaStream_t>(stream)),
+                                "pack kernel launch");
+                   }
+                 });
+}
+
 int fb_integrate_mesh_async(const fb_variant* vp, const fb_mesh_view* mesh, const double* coefficients,
                             void* out, int64_t out_len, int64_t* status, void* stream, fb_error* err)
 {

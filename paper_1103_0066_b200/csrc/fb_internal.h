@@ -14,7 +14,8 @@ namespace fbk {
 constexpr int kThreads = 288;
 constexpr int kTile = 288;  // element slots per CTA tile
 
-enum Op { kLaplacian = 0, kElasticity = 1, kWeighted = 2 };
+enum Op { kLaplacian = 0, kElasticity = 1, kWeighted = 2,
+          kPack = 3 };  // kPack: the sparse kernel emitting G itself (GPU pack_geometry)
 enum Mode { kStrict = 0, kFast = 1 };
 // kSparseSym: K validated to the P1 zero pattern, symmetric, and (elasticity)
 //             equal component-diagonal blocks -> nb(nb+1)/2 contractions.

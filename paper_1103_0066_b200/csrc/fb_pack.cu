@@ -9,27 +9,29 @@ std::atomic<long long>& launch_counter()
   return counter;
 }
 
+// GPU pack_geometry (src/geometry.cpp:312-351) = the sparse kernel's
+// warp-tile pipeline with G itself as the per-slot output (OP = kPack):
+// prefetched gathers, FP64 geometry with the reference's exact zero signs,
+// staged coalesced / bulk-TMA stores of the slot-major PackedGeometry.
+template <class S, int DIM>
+cudaError_t go_pack(const LaunchArgs& a, cudaStream_t st)
+{
+  KParamBlob kb{};
+  LaunchSpec s;
+  s.op = kPack;
+  s.dim = DIM;
+  // staged stores need a 16-byte aligned destination; else per-lane stores
+  s.staged = (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0 ? 3 : kStDirect;
+  return go_store<S, DIM, kPack, kStrict, false, false, false>(s, a, kb, st);
+}
+
 cudaError_t launch_pack(int dim, int prec, const LaunchArgs& a, cudaStream_t st)
 {
   if (a.nloc <= 0)
     return cudaSuccess;
-  const unsigned grid = (unsigned)num_tiles(a.nloc);
   if (prec == 0)
-  {
-    if (dim == 2)
-      fb_pack_geometry_kernel<float, 2><<<grid, kThreads, 0, st>>>(a);
-    else
-      fb_pack_geometry_kernel<float, 3><<<grid, kThreads, 0, st>>>(a);
-  }
-  else
-  {
-    if (dim == 2)
-      fb_pack_geometry_kernel<double, 2><<<grid, kThreads, 0, st>>>(a);
-    else
-      fb_pack_geometry_kernel<double, 3><<<grid, kThreads, 0, st>>>(a);
-  }
-  launch_counter().fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+    return dim == 2 ? go_pack<float, 2>(a, st) : go_pack<float, 3>(a, st);
+  return dim == 2 ? go_pack<double, 2>(a, st) : go_pack<double, 3>(a, st);
 }
 
 }  // namespace fbk

@@ -295,6 +295,16 @@ def integrate_packed_async(variant: KernelVariant, g, num_elements: int, out, st
     L.raise_for(rc, err)
 
 
+def pack_geometry_async(vertices, cells, dim: int, g_out, status, element_batch_size: int = 128,
+                        precision: str = "f64", stream: int = 0):
+    """Enqueue the GPU pack_geometry kernel on ``stream`` (device tensors only)."""
+    mv = mesh_view(vertices, cells, dim)
+    err = L.fb_error()
+    rc = L.load().fb_pack_geometry_async(C.byref(mv), element_batch_size, _prec(precision), _ptr(g_out),
+                                         _numel(g_out), _ptr(status), C.c_void_p(stream), C.byref(err))
+    L.raise_for(rc, err)
+
+
 def status_reset(status, stream: int = 0):
     err = L.fb_error()
     L.raise_for(L.load().fb_status_reset(_ptr(status), C.c_void_p(stream), C.byref(err)), err)

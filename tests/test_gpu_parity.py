@@ -280,6 +280,52 @@ def test_variant_invariance_bitwise():
                         assert got[: ne * 9].tobytes() == base[: ne * 9].tobytes()
 
 
+@pytest.mark.parametrize("dim,n", [(2, 30), (3, 9)])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_pack_geometry_async_bitwise(restatement, dim, n, prec):
+    import torch
+
+    v, c = mesh(dim, n)
+    ne = c.size // (dim + 1)
+    want = restatement.pack_geometry(v, c, dim, 32, prec)
+    g = torch.empty(want.size, dtype=torch.float32 if prec == "f32" else torch.float64, device="cuda")
+    st = torch.empty(2, dtype=torch.int64, device="cuda")
+    sid = torch.cuda.current_stream().cuda_stream
+    fb.status_reset(st, sid)
+    fb.pack_geometry_async(torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda(), dim, g, st, 32, prec, sid)
+    fb.status_check(st, sid)
+    assert g.cpu().numpy().tobytes() == want.tobytes()
+    assert ne > 0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_unaligned_device_outputs(restatement, prec):
+    """Caller buffers that are scalar- but not 16-byte-aligned take the
+    per-lane store path (scalar stores) and give the same bits."""
+    import torch
+
+    dt = torch.float32 if prec == "f32" else torch.float64
+    st = torch.empty(2, dtype=torch.int64, device="cuda")
+    sid = torch.cuda.current_stream().cuda_stream
+    for op, dim, n in (("laplacian", 3, 6), ("elasticity", 2, 12)):
+        v, c = mesh(dim, n)
+        dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+        var = fb.make_variant(op, dim, prec, "strict", element_batch_size=8)
+        ne = c.size // (dim + 1)
+        want = restatement.integrate_mesh(op, v, c, dim, bs=8, precision=prec)
+        buf = torch.empty(var.store_length(ne) + 1, dtype=dt, device="cuda")
+        out = buf[1:]
+        fb.status_reset(st, sid)
+        fb.integrate_mesh_async(var, dv, dc, out, st, sid)
+        fb.status_check(st, sid)
+        assert out.cpu().numpy().tobytes() == want.tobytes()
+        gwant = restatement.pack_geometry(v, c, dim, 8, prec)
+        gbuf = torch.empty(gwant.size + 1, dtype=dt, device="cuda")
+        fb.pack_geometry_async(dv, dc, dim, gbuf[1:], st, 8, prec, sid)
+        fb.status_check(st, sid)
+        assert gbuf[1:].cpu().numpy().tobytes() == gwant.tobytes()
+
+
 def test_launch_counter_counts_kernels():
     v, c = mesh(2, 4)
     var = fb.make_variant("laplacian", 2, "f64")
