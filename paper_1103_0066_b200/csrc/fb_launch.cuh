@@ -14,7 +14,8 @@ std::atomic<long long>& launch_counter();
 // Persistent grid: every resident CTA slot on the device, capped by the tile
 // count (cached per kernel instantiation; all devices in a box are B200s).
 template <class F>
-unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std::atomic<int>& slots)
+unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std::atomic<int>& slots,
+                         int cap_per_sm = 1 << 20)
 {
   int per = slots.load(std::memory_order_relaxed);
   if (per == 0)
@@ -24,6 +25,7 @@ unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std:
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    blocks = blocks < cap_per_sm ? blocks : cap_per_sm;
     per = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
     slots.store(per, std::memory_order_relaxed);
   }
@@ -53,7 +55,8 @@ cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st
   static std::atomic<int> slots{0};  // one cache per kernel instantiation
   constexpr int threads = kWarpsPerCta * 32;
   const int64_t nctas = (a.nloc + threads - 1) / threads;
-  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots), threads, smem, st>>>(a, kp, tm);
+  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots, sparse_cta_cap<DIM, OP>()), threads, smem, st>>>(
+      a, kp, tm);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
