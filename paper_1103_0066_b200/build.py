@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB
     srcs = [os.path.join(CSRC, s) for s in CU_SOURCES + CU_HOST_SOURCES + CPP_SOURCES + HEADERS] + PUBLIC_HEADERS
     if not force and os.path.exists(out) and os.path.getmtime(out) >= _newest(srcs + [__file__]):
         return out
-    build_dir = BUILD if out == LIB else BUILD + "_" + os.path.basename(out).replace(".so", "")
+    # A/B builds keep their objects out of the repo snapshot
+    build_dir = BUILD if out == LIB else os.path.join("/tmp", "fembatch_build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(build_dir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
     inc = ["-I", CSRC, "-I", os.path.join(ROOT, "include")]
