@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 import numpy as np
 
@@ -225,6 +226,7 @@ class Reference:
     def __init__(self, path: str = LIB_REFERENCE):
         if not os.path.exists(path):
             raise FileNotFoundError(path)
+        self.path = path
         self.lib = C.CDLL(path)
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
@@ -250,6 +252,23 @@ class Reference:
     def _check(self, rc):
         if rc != 0:
             raise OracleError(self.lib.ref_last_error().decode())
+
+    def write_files(self, op, dim, n, jitter, seed, bs, ce, precision, store_path, mesh_path):
+        """The reference's FBEMAT01 store file and text mesh file (golden F4
+        fixtures).  Run in a fresh interpreter that has not imported numpy:
+        the reference's iostream writers crash inside a numpy process here."""
+        import subprocess
+
+        code = ("import ctypes as C, sys\n"
+                f"L = C.CDLL({self.path!r})\n"
+                "f = L.ref_write_files\n"
+                "f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int, C.c_int,"
+                " C.c_char_p, C.c_char_p]\n"
+                f"sys.exit(f({op_id(op)}, {dim}, {n}, {float(jitter)!r}, {int(seed)}, {bs}, {ce}, "
+                f"{_prec(precision)}, {store_path.encode()!r}, {mesh_path.encode()!r}) != 0)\n")
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise OracleError(f"ref_write_files failed: {r.stderr.strip()}")
 
     def make_mesh(self, dim, n, jitter=0.0, seed=42):
         nv, ne = _i64(), _i64()

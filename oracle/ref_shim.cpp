@@ -7,6 +7,7 @@
 // baseline / `bench.py --impl reference` arm.  Nothing here is part of the
 // product library.
 #include <chrono>
+#include <fstream>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -189,6 +190,33 @@ int ref_integrate_mesh(int op, int dim, const double* v, std::int64_t nv,
     }
     copy_store(integrate_batches(var, g, wp, workers), out);
     return 0;
+  }
+  catch (const std::exception& e)
+  {
+    return fail(e);
+  }
+}
+
+// The reference's own FBEMAT01 store file (src/engine.cpp:413-508) and text
+// mesh file (src/geometry.cpp:353-395) for a structured (jittered) mesh --
+// golden files for the F4 format rows.
+int ref_write_files(int op, int dim, int n, double jitter, std::uint64_t seed, int bs, int ce, int precision,
+                    const char* store_path, const char* mesh_path)
+{
+  try
+  {
+    Mesh m = structured_simplicial_mesh(dim, n);
+    if (jitter > 0.0)
+      m = jitter_mesh(m, jitter, seed);
+    const FormSpec spec = make_form_spec(static_cast<Operator>(op), dim);
+    const KernelConfig cfg = config_from(bs, ce, 1, 0, precision);
+    const KernelVariant var = specialize_kernel(spec, build_analytic_tensor(spec.op, dim), cfg);
+    const ElementMatrixStore store = integrate_batches(var, pack_geometry(m, cfg));
+    std::ofstream fs(store_path, std::ios::binary);
+    write_store(fs, store);
+    std::ofstream fm(mesh_path);
+    write_mesh_text(fm, m);
+    return fs.good() && fm.good() ? 0 : -1;
   }
   catch (const std::exception& e)
   {

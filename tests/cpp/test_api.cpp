@@ -7,6 +7,8 @@
 //   test_api all   -- plus the GPU integration cases (needs a CUDA device)
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <iterator>
 #include <cstring>
 #include <functional>
 #include <sstream>
@@ -372,6 +374,63 @@ TEST_CASE(store_round_trip, true)
   CHECK_THROWS_AS(read_store(junk), std::runtime_error);
 }
 
+std::string g_golden = "tests/golden";  // argv[2]: the golden-file directory
+
+std::string slurp(const std::string& path)
+{
+  std::ifstream f(path, std::ios::binary);
+  return std::string(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+}
+
+struct RefFile {
+  const char* name;
+  Operator op;
+  int bs, ce;
+  Precision p;
+};
+const RefFile kRefFiles[] = {{"ref_store_2d_elasticity_f32", Operator::elasticity, 8, 2, Precision::f32},
+                             {"ref_store_3d_laplacian_f64", Operator::laplacian, 16, 1, Precision::f64}};
+
+// F4 formats against files the UNMODIFIED reference wrote
+// (tests/golden/make_golden.py): FBEMAT01 store (src/engine.cpp:413-508) and
+// text mesh (src/geometry.cpp:353-395) read back and re-written byte for byte.
+TEST_CASE(reference_written_files_round_trip, false)
+{
+  for (const RefFile& f : kRefFiles)
+  {
+    const std::string sbytes = slurp(g_golden + "/" + f.name + ".fbemat");
+    const std::string mtext = slurp(g_golden + "/" + f.name + ".mesh");
+    CHECK(!sbytes.empty() && !mtext.empty());
+    std::istringstream si(sbytes);
+    const ElementMatrixStore s = read_store(si);
+    CHECK(s.precision == f.p && s.element_batch_size == f.bs && s.num_concurrent_elements == f.ce);
+    std::ostringstream so;
+    write_store(so, s);
+    CHECK(so.str() == sbytes);
+    std::istringstream mi(mtext);
+    const Mesh m = read_mesh_text(mi);
+    CHECK(s.num_elements == m.num_elements() && s.dim == m.dim);
+    std::ostringstream mo;
+    write_mesh_text(mo, m);
+    CHECK(mo.str() == mtext);
+  }
+}
+
+// ... and the GPU engine reproduces the reference's store file exactly from
+// the reference's mesh file.
+TEST_CASE(gpu_store_equals_reference_file_bytes, true)
+{
+  for (const RefFile& f : kRefFiles)
+  {
+    std::istringstream mi(slurp(g_golden + "/" + f.name + ".mesh"));
+    const Mesh m = read_mesh_text(mi);
+    const ElementMatrixStore s = integrate(f.op, m, config_of(f.bs, f.ce, true, false, f.p));
+    std::ostringstream so;
+    write_store(so, s);
+    CHECK(so.str() == slurp(g_golden + "/" + f.name + ".fbemat"));
+  }
+}
+
 TEST_CASE(assembly_plan_pattern_and_validation, false)
 {
   const Mesh mesh = structured_simplicial_mesh(2, 2);  // 9 vertices, 8 triangles
@@ -436,6 +495,8 @@ TEST_CASE(global_assembly_is_the_serial_element_sum, true)
 int main(int argc, char** argv)
 {
   const bool gpu = argc > 1 && std::strcmp(argv[1], "all") == 0;
+  if (argc > 2)
+    g_golden = argv[2];
   int ran = 0;
   for (const Case& c : cases())
   {

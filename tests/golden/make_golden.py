@@ -26,6 +26,9 @@ from oracle.oracle import OPS, Reference  # noqa: E402
 # (tests/test_engine.cpp:135, acceptance.cpp:101-102 scaled down).
 MESHES = {"m2": (2, 4, 0.15, 42), "m3": (3, 2, 0.15, 42), "m2b": (2, 5, 0.15, 9)}
 BS = {"m2": 16, "m3": 7, "m2b": 128}
+# FBEMAT01 + text-mesh golden files: name -> (op, dim, n, jitter, bs, ce, precision)
+FILES = {"ref_store_2d_elasticity_f32": ("elasticity", 2, 3, 0.15, 8, 2, 0),
+         "ref_store_3d_laplacian_f64": ("laplacian", 3, 2, 0.15, 16, 1, 1)}
 
 
 def main():
@@ -59,9 +62,14 @@ def main():
         g[s * 4 + 0] = g[s * 4 + 3] = c
     out["synthetic_G"] = g
     out["synthetic_store"] = ref.integrate_packed("laplacian", 2, g, 5, 4, 1, ce=2)
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+    here = os.path.dirname(os.path.abspath(__file__))
+    path = os.path.join(here, "golden.npz")
     np.savez_compressed(path, **out)
     print(path, sum(a.nbytes for a in out.values()), "bytes raw")
+    # F4 formats: the reference's own FBEMAT01 store files and text mesh files
+    for name, (op, dim, n, jit, bs, ce, prec) in FILES.items():
+        ref.write_files(op, dim, n, jit, 42, bs, ce, prec, os.path.join(here, f"{name}.fbemat"),
+                        os.path.join(here, f"{name}.mesh"))
 
 
 if __name__ == "__main__":

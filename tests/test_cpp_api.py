@@ -7,6 +7,7 @@ import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BIN = os.path.join(HERE, "cpp", "_bin", "test_api")
+GOLDEN = os.path.join(HERE, "golden")
 CBIN = os.path.join(HERE, "cpp", "_bin", "test_c_abi")
 
 
@@ -17,14 +18,14 @@ def _binary(path=BIN):
 
 
 def test_cpp_api_host_cases():
-    r = subprocess.run([_binary(), "cpu"], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([_binary(), "cpu", GOLDEN], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
 
 
 @pytest.mark.gpu
 def test_cpp_api_gpu_cases():
-    r = subprocess.run([_binary(), "all"], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([_binary(), "all", GOLDEN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
 
