@@ -11,6 +11,7 @@
 #include <array>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <limits>
@@ -255,7 +256,14 @@ void element_window(const Job& j, int64_t s0, int64_t s1, int64_t& lo, int64_t& 
 }
 
 // Kernels index slots with 32-bit locals: split launches at 2^30 slots.
-constexpr int64_t kMaxLaunchSlots = int64_t(1) << 30;
+// FB_TEST_MAX_LAUNCH_SLOTS (environment, test hook) lowers the split so the
+// multi-launch path is exercised at small sizes.
+const int64_t kMaxLaunchSlots = []
+{
+  const char* e = std::getenv("FB_TEST_MAX_LAUNCH_SLOTS");
+  const long long v = e ? std::atoll(e) : 0;
+  return v >= 32 && v < (1ll << 30) ? static_cast<int64_t>(v / 32 * 32) : int64_t(1) << 30;
+}();
 
 void launch_integrate_chunked(const fbk::LaunchSpec& spec, const fbk::LaunchArgs& a, const fbk::KParamBlob& kp,
                               int nk, int dd, size_t ss, cudaStream_t st)
