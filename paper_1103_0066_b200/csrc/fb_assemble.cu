@@ -154,16 +154,24 @@ __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kerne
         for (int c = 0; c < NCW; ++c)
           vals[row + k * NC + c] = S(0);
     const int64_t q0 = __ldg(a.goff + g), q1 = __ldg(a.goff + g + 1);
-    for (int64_t q = q0 + lane; q < q1; q += 32 * U)
+    // the plan entries of chunk i+1 are loaded while chunk i's element rows
+    // are gathered and added (one exposed latency per chunk, not two)
+    uint32_t pk[U], ps[U];
+    auto load_plan = [&](int64_t q, uint32_t (&k)[U], uint32_t (&p)[U])
     {
-      uint32_t pk[U], ps[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
       {
         const int64_t qu = q + 32 * u;
-        pk[u] = qu < q1 ? __ldg(a.spk + qu) : kPad;
-        ps[u] = qu < q1 ? __ldg(a.spos + qu) : 0u;
+        k[u] = qu < q1 ? __ldg(a.spk + qu) : kPad;
+        p[u] = qu < q1 ? __ldg(a.spos + qu) : 0u;
       }
+    };
+    load_plan(q0 + lane, pk, ps);
+    for (int64_t q = q0 + lane; q < q1; q += 32 * U)
+    {
+      uint32_t npk[U], nps[U];
+      load_plan(q + 32 * U, npk, nps);
       S r[U][NB * NCW];
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -214,6 +222,12 @@ __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kerne
                 base[at[b * NCW + c]] = add_rn(base[at[b * NCW + c]], r[u][b + c * NB]);
           }
         }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+      {
+        pk[u] = npk[u];
+        ps[u] = nps[u];
+      }
     }
     if (in_smem)
       for (int k = 0; k < deg; ++k)
