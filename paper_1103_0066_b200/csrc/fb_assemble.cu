@@ -45,6 +45,9 @@ struct AsmShape {
   static constexpr int WARPS = NCW == 1 ? 4 : 2;
   static constexpr int SLOTS = NCW == 1 ? 32 : 24;
   static constexpr int U = NCW == 1 ? FB_ASM_U : 4;
+  // prefetch the next chunk's plan entries (registers: 3D elasticity FP64,
+  // already at the register limit, is faster without -- A/B measured)
+  static constexpr bool PREF = !(NC == 3 && sizeof(S) == 8);
   // batch the slot updates of one incidence (all loads, adds, stores): faster
   // in FP32, slower in FP64 (register pressure) -- A/B measured
   static constexpr bool BATCH = sizeof(S) == 4;
@@ -171,7 +174,8 @@ __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kerne
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
       uint32_t npk[U], nps[U];
-      load_plan(q + 32 * U, npk, nps);
+      if constexpr (Sh::PREF)
+        load_plan(q + 32 * U, npk, nps);
       S r[U][NB * NCW];
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -222,12 +226,17 @@ __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kerne
                 base[at[b * NCW + c]] = add_rn(base[at[b * NCW + c]], r[u][b + c * NB]);
           }
         }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
+      if constexpr (Sh::PREF)
       {
-        pk[u] = npk[u];
-        ps[u] = nps[u];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+        {
+          pk[u] = npk[u];
+          ps[u] = nps[u];
+        }
       }
+      else
+        load_plan(q + 32 * U, pk, ps);
     }
     if (in_smem)
       for (int k = 0; k < deg; ++k)
