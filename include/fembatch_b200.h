@@ -226,9 +226,11 @@ int fb_status_check(const int64_t* status, void* stream, fb_error* err);
  * read; padding slots are ignored. */
 typedef struct fb_assembly fb_assembly;
 
-/* cells: host or device pointer (num_elements*(dim+1) int32).  Errors:
- * out-of-range vertex id or a repeated vertex within a cell
- * (FB_ERR_INVALID_ARGUMENT, err->cell = the cell), vertex degree > 255. */
+/* cells: host or device pointer (num_elements*(dim+1) int32).  Device
+ * connectivity builds the plan on that GPU, host connectivity on the host
+ * (multithreaded); both give the same plan.  Errors: out-of-range vertex id
+ * or a repeated vertex within a cell (FB_ERR_INVALID_ARGUMENT, err->cell =
+ * the lowest such cell), vertex degree > 255. */
 fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t num_elements,
                                 int64_t num_vertices, fb_error* err);
 void fb_assembly_free(fb_assembly* a);

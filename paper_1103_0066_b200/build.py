@@ -30,6 +30,7 @@ CU_SOURCES = [
     "fb_kernels_f64_3d.cu",
     "fb_pack.cu",
     "fb_assemble.cu",
+    "fb_plan.cu",
 ]
 CPP_SOURCES = ["fb_capi.cpp", "fb_assembly.cpp", "fb_host.cpp", "fembatch_api.cpp"]
 CU_HOST_SOURCES = ["fb_tma.cpp"]  # host code that includes the kernel headers (nvcc)

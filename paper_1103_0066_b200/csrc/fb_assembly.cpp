@@ -1,7 +1,9 @@
 // fb_assembly.cpp -- extern "C" global assembly (include/fembatch_b200.h,
-// "global assembly"): the host-side plan (CSR pattern + vertex->element
-// incidence lists, built once per mesh, multithreaded) and the launch of the
-// deterministic gather kernel (fb_assemble.cu).
+// "global assembly"): the plan (CSR pattern + vertex->element incidence
+// lists, built once per mesh -- on the GPU for device-resident connectivity
+// (fb_plan.cu), else on the host, multithreaded; the two are array-for-array
+// identical) and the launch of the deterministic gather kernel
+// (fb_assemble.cu).
 //
 // Plan construction:
 //   1. incidences by counting sort over elements in ascending order, so each
@@ -31,6 +33,7 @@ struct DevPlan {
   uint32_t* spk = nullptr;
   uint32_t* spos = nullptr;
   int64_t* nbr_ptr = nullptr;
+  int32_t* nbr = nullptr;  // only on the device that built the plan
 };
 
 }  // namespace
@@ -45,10 +48,12 @@ struct fb_assembly {
   // device layout (SELL-32, fb_internal.h AsmArgs)
   std::vector<int64_t> goff;
   std::vector<uint32_t> spk, spos;
+  int64_t total_nbr = 0;  // sum of vertex degrees
+  int home = -1;          // device that built the plan (host arrays filled lazily), -1 = host-built
   mutable std::mutex mu;
   mutable std::map<int, DevPlan> dev;
   int64_t rows() const { return nv * nc; }
-  int64_t nnz() const { return nbr_ptr.empty() ? 0 : nbr_ptr[nv] * nc * nc; }
+  int64_t nnz() const { return total_nbr * nc * nc; }
   ~fb_assembly()
   {
     int cur = 0;
@@ -60,6 +65,7 @@ struct fb_assembly {
       cudaFree(p.spk);
       cudaFree(p.spos);
       cudaFree(p.nbr_ptr);
+      cudaFree(p.nbr);
     }
     cudaSetDevice(cur);
   }
@@ -145,6 +151,7 @@ void build_plan(fb_assembly& A, const int32_t* cells)
     A.nbr_ptr[v + 1] = A.nbr_ptr[v] + deg[v];
   }
   A.nbr.resize(A.nbr_ptr[nv]);
+  A.total_nbr = A.nbr_ptr[nv];
   {
     std::vector<std::pair<int64_t, size_t>> order;
     for (size_t t = 0; t < chunk_nbr.size(); ++t)
@@ -204,6 +211,41 @@ void build_plan(fb_assembly& A, const int32_t* cells)
                });
 }
 
+void build_plan_gpu(fb_assembly& A, const int32_t* cells, int dev)
+{
+  int cur = 0;
+  cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+  cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  cudaStream_t st = nullptr;
+  cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+  fbk::PlanDevice P;
+  int64_t bad[3];
+  const cudaError_t e = fbk::build_plan_device(A.dim, A.ne, A.nv, cells, st, &P, bad);
+  cudaStreamDestroy(st);
+  cudaSetDevice(cur);
+  cuda_check(e, "assembly plan build");
+  DevPlan p;
+  p.goff = P.goff;
+  p.spk = P.spk;
+  p.spos = P.spos;
+  p.nbr_ptr = P.nbr_ptr;
+  p.nbr = P.nbr;
+  if (bad[0] >= 0 || bad[1] >= 0)
+  {
+    const bool range = bad[0] >= 0 && (bad[1] < 0 || bad[0] < bad[1]);
+    const int64_t c = range ? bad[0] : bad[1];
+    throw_code(FB_ERR_INVALID_ARGUMENT,
+               (range ? "cell vertex index out of range in cell " : "repeated vertex in cell ") + std::to_string(c), c);
+  }
+  A.home = dev;
+  A.dev.emplace(dev, p);  // owned from here on (freed by ~fb_assembly)
+  A.total_nbr = P.total_nbr;
+  if (bad[2] >= 0)
+    throw_code(FB_ERR_INVALID_ARGUMENT, "vertex degree exceeds 255 at vertex " + std::to_string(bad[2]), -1);
+  if (A.total_nbr * A.nc > INT32_MAX || A.rows() > INT32_MAX)
+    throw_code(FB_ERR_INVALID_ARGUMENT, "assembled operator exceeds 32-bit column indices", -1);
+}
+
 template <class T>
 T* upload(const std::vector<T>& h)
 {
@@ -214,12 +256,41 @@ T* upload(const std::vector<T>& h)
   return d;
 }
 
+template <class T>
+void download(std::vector<T>& h, const T* d, int64_t n)
+{
+  h.resize(n);
+  if (n > 0)
+    cuda_check(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost), "cudaMemcpy plan");
+}
+
+// Host copies of a device-built plan (for the pattern, or another device).
+// Caller holds A.mu.
+void ensure_host(const fb_assembly& A)
+{
+  if (A.home < 0 || !A.nbr_ptr.empty())
+    return;
+  auto& M = const_cast<fb_assembly&>(A);
+  const DevPlan& p = A.dev.at(A.home);
+  int cur = 0;
+  cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+  cuda_check(cudaSetDevice(A.home), "cudaSetDevice");
+  const int64_t ngroups = (A.nv + 31) / 32;
+  download(M.goff, p.goff, ngroups + 1);
+  download(M.spk, p.spk, M.goff.back());
+  download(M.spos, p.spos, M.goff.back());
+  download(M.nbr, p.nbr, A.total_nbr);
+  download(M.nbr_ptr, p.nbr_ptr, A.nv + 1);
+  cuda_check(cudaSetDevice(cur), "cudaSetDevice");
+}
+
 const DevPlan& plan_on(const fb_assembly& A, int dev)
 {
   std::lock_guard<std::mutex> lock(A.mu);
   auto it = A.dev.find(dev);
   if (it != A.dev.end())
     return it->second;
+  ensure_host(A);
   DevPlan p;
   p.goff = upload(A.goff);
   p.spk = upload(A.spk);
@@ -292,17 +363,11 @@ fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t n
                            A->nc = op == FB_ELASTICITY ? dim : 1;
                            A->nv = nv;
                            A->ne = ne;
-                           std::vector<int32_t> host;
-                           const int32_t* c = cells;
-                           if (ne > 0 && pointer_device(cells) >= 0)
-                           {
-                             host.resize(ne * (dim + 1));
-                             cuda_check(cudaMemcpy(host.data(), cells, host.size() * sizeof(int32_t),
-                                                   cudaMemcpyDeviceToHost),
-                                        "cudaMemcpy cells");
-                             c = host.data();
-                           }
-                           build_plan(*A, c);
+                           const int cdev = ne > 0 ? pointer_device(cells) : -1;
+                           if (cdev >= 0)
+                             build_plan_gpu(*A, cells, cdev);  // device-resident connectivity
+                           else
+                             build_plan(*A, cells);
                          });
   return rc == FB_OK ? A.release() : nullptr;
 }
@@ -321,6 +386,10 @@ int fb_assembly_pattern(const fb_assembly* a, int64_t* row_ptr, int64_t row_ptr_
                      invalid("null assembly plan");
                    if (row_ptr_len != a->rows() + 1 || nnz != a->nnz())
                      invalid("pattern buffers must hold rows+1 offsets and nnz columns");
+                   {
+                     std::lock_guard<std::mutex> lock(a->mu);
+                     ensure_host(*a);
+                   }
                    const int nc = a->nc;
                    int64_t z = 0;
                    row_ptr[0] = 0;

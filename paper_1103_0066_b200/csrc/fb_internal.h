@@ -86,6 +86,22 @@ struct AsmArgs {
 };
 cudaError_t launch_assemble(int dim, int nc, int prec, const AsmArgs&, cudaStream_t);
 
+// The same plan built on the GPU from device-resident connectivity
+// (fb_plan.cu); arrays are stream-ordered allocations the caller frees with
+// cudaFree.  bad[0] = lowest cell with an out-of-range id, bad[1] = lowest
+// cell with a repeated vertex, bad[2] = lowest vertex of degree > 255 (-1 =
+// none); on bad[0|1] nothing is allocated, on bad[2] only the offsets.
+struct PlanDevice {
+  int64_t* goff = nullptr;
+  uint32_t* spk = nullptr;
+  uint32_t* spos = nullptr;
+  int64_t* nbr_ptr = nullptr;
+  int32_t* nbr = nullptr;
+  int64_t total_nbr = 0, total_sell = 0;
+};
+cudaError_t build_plan_device(int dim, int64_t ne, int64_t nv, const int32_t* cells, cudaStream_t st,
+                              PlanDevice* out, int64_t* bad);
+
 inline cudaError_t launch_integrate(const LaunchSpec& s, const LaunchArgs& a,
                                     const KParamBlob& k, cudaStream_t st)
 {

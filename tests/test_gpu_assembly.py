@@ -80,6 +80,44 @@ def test_assembly_shuffled_cells_and_unreferenced_vertices(restatement):
         assert plan.assemble(var, store, symmetric=True).tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("op,dim,n", [("laplacian", 2, 7), ("elasticity", 3, 4), ("weighted-laplacian", 3, 3)])
+def test_gpu_built_plan_equals_host_plan(op, dim, n):
+    import torch
+
+    v, c = fb.structured_mesh(dim, n, 0.15, 42)
+    nv = v.size // dim
+    cs = c.reshape(-1, dim + 1)[np.random.default_rng(5).permutation(c.size // (dim + 1))].ravel().copy()
+    for cells in (c, cs):
+        host = fb.AssemblyPlan(op, dim, cells, nv)
+        dev = fb.AssemblyPlan(op, dim, torch.from_numpy(cells).cuda(), nv)
+        assert dev.rows == host.rows and dev.nnz == host.nnz
+        for a, b in zip(dev.pattern(), host.pattern()):
+            assert np.array_equal(a, b)
+        var = fb.make_variant(op, dim, "f64", "strict", element_batch_size=32)
+        w = None
+        if op == "weighted-laplacian":
+            w = np.ascontiguousarray(1.0 + v.reshape(-1, dim)[cells.reshape(-1, dim + 1), 0].ravel())
+        store = torch.from_numpy(fb.integrate_mesh(var, v, cells, w)).cuda()
+        assert torch.equal(dev.assemble(var, store), host.assemble(var, store))
+
+
+def test_gpu_built_plan_rejects_bad_connectivity():
+    import torch
+
+    v, c = fb.structured_mesh(3, 2)
+    nv = v.size // 3
+    bad = c.copy()
+    bad[4 * 7 + 2] = -1
+    bad[4 * 9 + 0] = nv + 5
+    with pytest.raises(_lib.InvalidArgument, match="out of range in cell 7") as ei:
+        fb.AssemblyPlan("laplacian", 3, torch.from_numpy(bad).cuda(), nv)
+    assert ei.value.cell == 7
+    rep = c.copy()
+    rep[4 * 3 + 1] = rep[4 * 3 + 3]
+    with pytest.raises(_lib.InvalidArgument, match="repeated vertex in cell 3"):
+        fb.AssemblyPlan("elasticity", 3, torch.from_numpy(rep).cuda(), nv)
+
+
 def _raise(plan, var, store):  # fb_assemble with an unknown flag bit
     err = _lib.fb_error()
     rc = plan._lib.fb_assemble(plan._h, var.handle, store.ctypes.data, store.size,
