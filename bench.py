@@ -353,7 +353,7 @@ def main():
         # global CSR assembly of the timed store (device-resident)
         asm = None
         if not args.no_assembly:
-            plan = fb.AssemblyPlan(op, dim, cells, v.size // dim)
+            plan = fb.AssemblyPlan(op, dim, dc, v.size // dim)  # plan built on the GPU
             vals = torch.empty(plan.nnz, dtype=tdt, device=dev)
             for _ in range(max(args.warmup, 1)):
                 plan.assemble_async(var, out, vals, sid, symmetric=var.path in (0, 3))
