@@ -78,7 +78,9 @@ def _properties(store, op, dim, ne):
 
 @pytest.mark.parametrize("op,dim,ne,jitter,prec", [
     ("laplacian", 3, 1 << 24, 0.15, "f32"),
+    ("laplacian", 3, 1 << 24, 0.15, "f64"),
     ("elasticity", 3, 1 << 23, 0.0, "f32"),
+    ("elasticity", 3, 1 << 23, 0.0, "f64"),
 ])
 def test_large_3d_sampled_bitwise_and_properties(restatement, op, dim, ne, jitter, prec):
     v, c, dv, dc = _device_mesh(dim, ne, jitter)
@@ -92,3 +94,20 @@ def test_large_3d_sampled_bitwise_and_properties(restatement, op, dim, ne, jitte
     want = restatement.integrate_mesh(op, v, cs, dim, bs=1, precision=prec).reshape(-1, kr2)
     got = store.view(-1, kr2)[torch.from_numpy(idx).cuda()].cpu().numpy()
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("op,dim,ne,prec,tol", [
+    ("laplacian", 3, 1 << 24, "f32", 5e-6),
+    ("elasticity", 2, 1 << 20, "f64", 1e-13),
+])
+def test_fast_mode_at_size_against_direct_oracle(restatement, op, dim, ne, prec, tol):
+    """Fast mode (FMA, one reciprocal of det) at a BASELINE size: sampled
+    elements within the stated normwise tolerance of the FP64 direct oracle."""
+    v, c, dv, dc = _device_mesh(dim, ne, 0.15)
+    store = fb.integrate_mesh(fb.make_variant(op, dim, prec, "fast"), dv, dc)
+    kr = krows(op, dim)
+    idx = _sample(ne)
+    got = store.view(-1, kr * kr)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    a = got.reshape(-1, kr, kr).transpose(0, 2, 1)
+    direct = restatement.direct_mesh(op, v, c, dim, elements=idx)
+    assert normwise_error(a, direct) <= tol
