@@ -20,3 +20,8 @@ for w in 2d-elasticity-1m 3d-laplacian-16m 3d-elasticity-8m; do
 done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_assemble -s 1 -c 1 \
     -o $o/${tag}_ncu_assemble_3d-laplacian-16m_f32 python tools/asmbench.py --workloads 3d-laplacian-16m --precisions f32 --steps 1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:fb_integrate_sparse<float, .int.3, .int.3," -s 1 -c 1 \
+    -o $o/${tag}_ncu_pack_geometry_3d_f32 python tools/pathbench.py --precisions f32 --steps 1 > /dev/null 2>&1
+timeout 500 python tools/asmbench.py > $o/${tag}_asmbench.txt 2>&1
+timeout 500 python tools/pathbench.py > $o/${tag}_pathbench.txt 2>&1
+timeout 300 python tools/kbench.py --modes strict,fast --steps 20 > $o/${tag}_kbench.txt 2>&1
