@@ -39,12 +39,18 @@ namespace {
 // in shared memory (<= 48 KB static per CTA); vertices with more neighbours
 // accumulate in their own rows of the output.  U = incidences in flight per
 // lane.
-template <class S, int NC>
+#ifndef FB_ASM_NCW2
+#define FB_ASM_NCW2 1
+#endif
+#ifndef FB_ASM_U2D
+#define FB_ASM_U2D FB_ASM_U
+#endif
+template <class S, int DIM, int NC>
 struct AsmShape {
-  static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : 1;
+  static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : 1);
   static constexpr int WARPS = NCW == 1 ? 4 : 2;
   static constexpr int SLOTS = NCW == 1 ? 32 : 24;
-  static constexpr int U = NCW == 1 ? FB_ASM_U : 4;
+  static constexpr int U = DIM == 2 ? FB_ASM_U2D : (NCW == 1 ? FB_ASM_U : 4);
   // prefetch the next chunk's plan entries (registers: 3D elasticity FP64,
   // already at the register limit, is faster without -- A/B measured)
   static constexpr bool PREF = !(NC == 3 && sizeof(S) == 8);
@@ -121,9 +127,9 @@ __device__ __forceinline__ void load_row(const S* blk, int i, int cj0, S (&r)[N]
 }
 
 template <class S, int DIM, int NC, bool SYM>
-__global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kernel(const AsmArgs a)
+__global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_kernel(const AsmArgs a)
 {
-  using Sh = AsmShape<S, NC>;
+  using Sh = AsmShape<S, DIM, NC>;
   constexpr int NB = DIM + 1, KROWS = NB * NC, NK = KROWS * KROWS;
   constexpr int NCW = Sh::NCW, NWC = NC / NCW;  // column components per warp, warps per row
   constexpr int T = 32 * Sh::WARPS;
@@ -248,8 +254,8 @@ __global__ void __launch_bounds__(32 * AsmShape<S, NC>::WARPS) fb_assemble_kerne
 template <class S, int DIM, int NC, bool SYM>
 cudaError_t go(const AsmArgs& a, cudaStream_t st)
 {
-  constexpr int T = 32 * AsmShape<S, NC>::WARPS;
-  const int64_t nwarps = (a.nv + 31) / 32 * NC * (NC / AsmShape<S, NC>::NCW);
+  constexpr int T = 32 * AsmShape<S, DIM, NC>::WARPS;
+  const int64_t nwarps = (a.nv + 31) / 32 * NC * (NC / AsmShape<S, DIM, NC>::NCW);
   if (nwarps <= 0)
     return cudaSuccess;
   static int grid_cap = 0;
