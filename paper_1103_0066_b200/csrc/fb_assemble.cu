@@ -40,7 +40,7 @@ namespace {
 // accumulate in their own rows of the output.  U = incidences in flight per
 // lane.
 #ifndef FB_ASM_NCW2
-#define FB_ASM_NCW2 1
+#define FB_ASM_NCW2 2  // 2D elasticity: a warp reads the whole element row (A/B: 1 is slower)
 #endif
 #ifndef FB_ASM_U2D
 #define FB_ASM_U2D FB_ASM_U
