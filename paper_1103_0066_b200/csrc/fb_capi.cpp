@@ -878,31 +878,6 @@ int fb_integrate_mesh_async(const fb_variant* vp, const fb_mesh_view* mesh, cons
                    fbk::LaunchSpec s = spec_of(v, false);
                    if (!aligned16(out))
                      s.staged = 0;
-#if FB_TEX
-                   // experiment only: one cached texture object for the last vertex buffer
-                   static const void* tex_ptr = nullptr;
-                   static int64_t tex_n = 0;
-                   static cudaTextureObject_t tex = 0;
-                   if (v.dim == 3 && a.nv > 0 && a.nv * 3 < (int64_t(1) << 27))
-                   {
-                     if (tex_ptr != a.vtx || tex_n != a.nv)
-                     {
-                       if (tex)
-                         cudaDestroyTextureObject(tex);
-                       cudaResourceDesc rd{};
-                       rd.resType = cudaResourceTypeLinear;
-                       rd.res.linear.devPtr = const_cast<double*>(a.vtx);
-                       rd.res.linear.desc = cudaCreateChannelDesc<int2>();
-                       rd.res.linear.sizeInBytes = a.nv * 3 * sizeof(double);
-                       cudaTextureDesc td{};
-                       td.readMode = cudaReadModeElementType;
-                       cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "cudaCreateTextureObject");
-                       tex_ptr = a.vtx;
-                       tex_n = a.nv;
-                     }
-                     a.vtx_tex = tex;
-                   }
-#endif
                    launch_integrate_chunked(s, a, v.kp, v.krows * v.krows, v.dim * v.dim,
                                             scalar_size(v.cfg.precision), static_cast<cudaStream_t>(stream));
                  });

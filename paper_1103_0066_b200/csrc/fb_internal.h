@@ -40,7 +40,6 @@ struct LaunchArgs {
   int64_t slot0 = 0;               // global slot index of local slot 0
   int cells_aligned16 = 0;
   int vtx_aligned16 = 0;
-  unsigned long long vtx_tex = 0;  // FB_TEX experiment: texture object over vtx (int2 texels), 0 = none
 };
 
 struct LaunchSpec {
