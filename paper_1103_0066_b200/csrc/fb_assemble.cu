@@ -142,27 +142,45 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   const int lane = threadIdx.x & 31;
   const int64_t ngroups = (a.nv + 31) / 32;
   const int64_t nwarps = ngroups * NC * NWC;
-  for (int64_t w = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); w < nwarps;
-       w += static_cast<int64_t>(gridDim.x) * (T / 32))
+  // task descriptors (row-block offsets of the lane's vertex, the group's
+  // plan range) are prefetched one task ahead, so a task's dependent chain
+  // is plan -> element rows -> adds, not offsets -> plan -> rows -> adds
+  struct Desc {
+    int64_t r0 = 0, r1 = 0, q0 = 0, q1 = 0;
+  };
+  auto load_desc = [&](int64_t w)
   {
+    Desc d;
+    const int64_t g = w / (NC * NWC);
+    const int64_t v = g * 32 + lane;
+    if (v < a.nv)
+    {
+      d.r0 = __ldg(a.nbr_ptr + v);
+      d.r1 = __ldg(a.nbr_ptr + v + 1);
+    }
+    d.q0 = __ldg(a.goff + g);
+    d.q1 = __ldg(a.goff + g + 1);
+    return d;
+  };
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * (T / 32);
+  int64_t w = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5);
+  Desc cur;
+  if (w < nwarps)
+    cur = load_desc(w);
+  for (; w < nwarps; w += wstride)
+  {
+    Desc nxt;
+    if (w + wstride < nwarps)
+      nxt = load_desc(w + wstride);
     const int64_t g = w / (NC * NWC);
     const int sub = static_cast<int>(w - g * (NC * NWC));
     const int ci = sub / NWC, cj0 = (sub % NWC) * NCW;
-    const int64_t v = g * 32 + lane;
-    const bool live = v < a.nv;
-    const int64_t r0 = live ? __ldg(a.nbr_ptr + v) : 0;
-    const int deg = live ? static_cast<int>(__ldg(a.nbr_ptr + v + 1) - r0) : 0;
+    const int64_t r0 = cur.r0;
+    const int deg = static_cast<int>(cur.r1 - cur.r0);
+    const int64_t q0 = cur.q0, q1 = cur.q1;
     // value (neighbour slot k, column component cj0 + c) at row + k*NC + c
     const int64_t row = r0 * NC * NC + static_cast<int64_t>(ci) * deg * NC + cj0;
     const bool in_smem = deg <= SLOTS;
-    if (in_smem)
-      for (int k = 0; k < deg * NCW; ++k)
-        acc[k * T] = S(0);
-    else
-      for (int k = 0; k < deg; ++k)
-        for (int c = 0; c < NCW; ++c)
-          vals[row + k * NC + c] = S(0);
-    const int64_t q0 = __ldg(a.goff + g), q1 = __ldg(a.goff + g + 1);
     // the plan entries of chunk i+1 are loaded while chunk i's element rows
     // are gathered and added (one exposed latency per chunk, not two)
     uint32_t pk[U], ps[U];
@@ -177,6 +195,14 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
       }
     };
     load_plan(q0 + lane, pk, ps);
+    // zero the accumulators while the plan entries are in flight
+    if (in_smem)
+      for (int k = 0; k < deg * NCW; ++k)
+        acc[k * T] = S(0);
+    else
+      for (int k = 0; k < deg; ++k)
+        for (int c = 0; c < NCW; ++c)
+          vals[row + k * NC + c] = S(0);
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
       uint32_t npk[U], nps[U];
@@ -248,6 +274,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
       for (int k = 0; k < deg; ++k)
         for (int c = 0; c < NCW; ++c)
           vals[row + k * NC + c] = acc[(k * NCW + c) * T];
+    cur = nxt;
   }
 }
 
