@@ -167,10 +167,13 @@ int fb_variant_path(const fb_variant* v);
  * reference computes them.  coefficients: num_elements*(dim+1) doubles for
  * the weighted form (reference CoefficientField), else NULL.
  *
- * devices/ndev: host pointers are sharded over these devices by contiguous
- * tile-aligned element ranges (no collectives; outputs concatenate).
- * NULL/0 means device 0 (or, for device pointers, the pointers' device).
- * Host buffers should be pinned for full PCIe bandwidth. */
+ * devices/ndev: the job is sharded over these devices by contiguous
+ * tile-aligned element ranges (no collectives; outputs concatenate).  Any
+ * buffer may be on the host or on any device: each shard device stages its
+ * own slice (a device-resident operand on another GPU moves by NVLink peer
+ * copy, e.g. all shards gathered into one device's store).  NULL/0 means
+ * device 0 (or, for device pointers, the pointers' device).  Host buffers
+ * should be pinned for full PCIe bandwidth. */
 int fb_integrate_mesh(const fb_variant* v, const fb_mesh_view* mesh,
                       const double* coefficients, void* out, int64_t out_len,
                       const int* devices, int ndev, fb_error* err);

@@ -317,7 +317,7 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
     else
     {
       double* d = static_cast<double*>(ctx.vtx.get(j.nv * j.dim * sizeof(double)));
-      cuda_check(cudaMemcpyAsync(d, j.vtx, j.nv * j.dim * sizeof(double), cudaMemcpyHostToDevice,
+      cuda_check(cudaMemcpyAsync(d, j.vtx, j.nv * j.dim * sizeof(double), cudaMemcpyDefault,
                                  ctx.st[0]),
                  "upload vertices");
       base.vtx = d;
@@ -362,7 +362,7 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
       {
         void* d = ctx.in[which].get((c1 - c0) * dd * ss);
         cuda_check(cudaMemcpyAsync(d, static_cast<const char*>(j.g) + c0 * dd * ss, (c1 - c0) * dd * ss,
-                                   cudaMemcpyHostToDevice, st),
+                                   cudaMemcpyDefault, st),
                    "upload G");
         a.g_in = d;
       }
@@ -375,7 +375,7 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
       {
         int32_t* d = static_cast<int32_t*>(ctx.in[which].get((hi - lo) * nb * sizeof(int32_t)));
         cuda_check(cudaMemcpyAsync(d, j.cells + lo * nb, (hi - lo) * nb * sizeof(int32_t),
-                                   cudaMemcpyHostToDevice, st),
+                                   cudaMemcpyDefault, st),
                    "upload cells");
         a.cells = d - lo * nb;
       }
@@ -389,7 +389,7 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
       {
         double* d = static_cast<double*>(ctx.coeff[which].get((hi - lo) * nb * sizeof(double)));
         cuda_check(cudaMemcpyAsync(d, j.coeffs + lo * nb, (hi - lo) * nb * sizeof(double),
-                                   cudaMemcpyHostToDevice, st),
+                                   cudaMemcpyDefault, st),
                    "upload coefficients");
         a.coeffs = d - lo * nb;
       }
@@ -405,7 +405,7 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
     launch(jj, a, st);
     if (!direct_out)
       cuda_check(cudaMemcpyAsync(static_cast<char*>(j.out) + c0 * j.nk * ss, dout, out_bytes,
-                                 cudaMemcpyDeviceToHost, st),
+                                 cudaMemcpyDefault, st),
                  "download store");
   }
   cuda_check(cudaEventRecord(ctx.ev, ctx.st[1]), "cudaEventRecord");
@@ -440,10 +440,10 @@ void run_job(const Job& j, const int* devices, int ndev)
   for (int d : devs)
     if (d < 0 || d >= have)
       invalid("device " + std::to_string(d) + " does not exist");
-  // device-resident operands must live on the (single) target device
-  for (int d : {j.out_dev, j.cells_dev, j.g_dev, j.vtx_dev, j.coeff_dev})
-    if (d >= 0 && (devs.size() != 1 || d != devs[0]))
-      invalid("device-resident buffers require a single target device that owns them");
+  // Operands may live on the host or on any device: each shard device works
+  // on its own slice and the staging copies use cudaMemcpyDefault, so a
+  // device-resident operand on another GPU moves over NVLink peer copies
+  // (e.g. every GPU's output slice gathered into one device's store).
   if (j.nslots == 0)
     return;
 
