@@ -166,28 +166,47 @@ class ClockSampler:
                 "samples": len(timed), "source": "nvml 2 ms polling inside the timed regions"}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(op, dim, prec, v, cells, target_s=10.0):
     """The reference's own CPU path (oracle/_ref) on this host's cores: the
     mesh-in / matrices-out composition pack_geometry + integrate_batches with
-    the paper's best variant (bs128 ce2 interleaved), all hardware threads."""
+    the paper's best variant (bs128 ce2 interleaved); workers = all hardware
+    threads and 1, the better reported, plus the
+    reference's integrate-only timing (include_packing=false) for context."""
     from oracle.oracle import Reference, Restatement, reference_available
 
     ne = cells.size // (dim + 1)
     flops = flops_per_element(op, dim) * ne
     cores = os.cpu_count() or 1
+    p = 0 if prec == "f32" else 1
     if reference_available():
         ref = Reference()
-        t1, _ = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True,
-                                   precision=0 if prec == "f32" else 1, workers=cores, reps=1,
-                                   include_packing=True)
-        reps = int(max(1, min(50, target_s / max(t1, 1e-6))))
-        tmin, tmean = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True,
-                                         precision=0 if prec == "f32" else 1, workers=cores, reps=reps,
-                                         include_packing=True)
-        return {"value": flops / tmin * 1e-9, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+        best = None
+        for workers in sorted({cores, 1}, reverse=True):
+            t1, _ = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True, precision=p,
+                                       workers=workers, reps=1, include_packing=True)
+            reps = int(max(1, min(50, target_s / 2 / max(t1, 1e-6))))
+            tmin, tmean = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True, precision=p,
+                                             workers=workers, reps=reps, include_packing=True)
+            if best is None or tmin < best[1]:
+                best = (workers, tmin, tmean, reps)
+        workers, tmin, tmean, reps = best
+        ti, _ = ref.time_integrate(op, v, cells, dim, bs=128, ce=2, interleave=True, precision=p,
+                                   workers=workers, reps=max(1, reps // 2), include_packing=False)
+        return {"value": flops / tmin * 1e-9, "unit": "GFLOP/s", "cores": workers, "kind": "reference",
                 "elements_per_s": ne / tmin, "seconds_min": tmin, "seconds_mean": tmean,
+                "integrate_only_gflops": flops / ti * 1e-9, "host_threads": cores, "cpu_model": cpu_model(),
                 "sample": f"full workload ({ne} elements) x {reps} reps, pack_geometry+integrate_batches, "
-                          f"bs128 ce2 interleaved, workers={cores}, min over reps"}
+                          f"bs128 ce2 interleaved, workers={workers} (best of {cores} and 1), min over reps"}
     ora = Restatement()
     sample = min(ne, 1 << 18)
     c = np.ascontiguousarray(cells[: sample * (dim + 1)])
@@ -195,7 +214,7 @@ def cpu_baseline(op, dim, prec, v, cells, target_s=10.0):
     ora.integrate_mesh(op, v, c, dim, bs=128, precision=prec)
     t = time.perf_counter() - t0
     return {"value": flops_per_element(op, dim) * sample / t * 1e-9, "unit": "GFLOP/s", "cores": 1,
-            "kind": "port", "elements_per_s": sample / t,
+            "kind": "port", "elements_per_s": sample / t, "cpu_model": cpu_model(),
             "sample": f"first {sample} elements, C restatement, 1 thread"}
 
 
