@@ -69,8 +69,23 @@ struct QuadratureRule {
   int num_points() const { return static_cast<int>(weights.size()); }
   double point(int q, int c) const { return points[static_cast<std::size_t>(q) * dim + c]; }
 };
+// P1 hat functions at the points of a rule: values [function][point],
+// reference gradients [function][point][direction] (constant per function).
+struct TabulatedBasis {
+  int dim = 0;
+  int num_basis_funcs = 0;
+  int num_points = 0;
+  std::vector<double> values;
+  std::vector<double> gradients;
+  double value(int f, int q) const { return values[static_cast<std::size_t>(f) * num_points + q]; }
+  double gradient(int f, int q, int d) const
+  {
+    return gradients[(static_cast<std::size_t>(f) * num_points + q) * dim + d];
+  }
+};
 ReferenceCell make_reference_cell(int dim);
 QuadratureRule make_quadrature(int dim, int degree);
+TabulatedBasis tabulate_p1_basis(const ReferenceCell& cell, const QuadratureRule& rule);
 
 // ---- forms (reference include/fembatch/forms.hpp) -------------------------
 enum class Operator { laplacian, elasticity, weighted_laplacian };

@@ -146,6 +146,34 @@ QuadratureRule make_quadrature(int dim, int degree)
   return r;
 }
 
+// phi_0 = 1 - sum(xi), phi_{d+1} = xi_d; gradients (-1, ..., -1) and e_d
+// (reference include/fembatch/reference.hpp:57-59).
+TabulatedBasis tabulate_p1_basis(const ReferenceCell& cell, const QuadratureRule& rule)
+{
+  if (cell.dim != rule.dim)
+    throw std::invalid_argument("cell and rule dimensions differ");
+  TabulatedBasis t;
+  t.dim = cell.dim;
+  t.num_basis_funcs = cell.dim + 1;
+  t.num_points = rule.num_points();
+  const std::size_t nq = static_cast<std::size_t>(t.num_points);
+  t.values.assign((cell.dim + 1) * nq, 0.0);
+  t.gradients.assign((cell.dim + 1) * nq * cell.dim, 0.0);
+  for (std::size_t q = 0; q < nq; ++q)
+  {
+    double rest = 1.0;
+    for (int d = 0; d < cell.dim; ++d)
+    {
+      rest -= rule.point(static_cast<int>(q), d);
+      t.values[(d + 1) * nq + q] = rule.point(static_cast<int>(q), d);
+      t.gradients[q * cell.dim + d] = -1.0;
+      t.gradients[((d + 1) * nq + q) * cell.dim + d] = 1.0;
+    }
+    t.values[q] = rest;
+  }
+  return t;
+}
+
 // -------------------------------------------------------------------- forms
 const char* operator_name(Operator op)
 {

@@ -31,6 +31,19 @@ FILES = {"ref_store_2d_elasticity_f32": ("elasticity", 2, 3, 0.15, 8, 2, 0),
          "ref_store_3d_laplacian_f64": ("laplacian", 3, 2, 0.15, 16, 1, 1)}
 
 
+def acceptance_criteria(text, which):
+    """The blocks of the acceptance report that belong to the given criteria."""
+    out, keep = [], False
+    for line in text.splitlines():
+        if line.startswith("[PASS] criterion ") or line.startswith("[FAIL] criterion "):
+            keep = int(line.split("criterion ")[1].split(":")[0]) in which
+        elif not line.startswith("    "):
+            keep = False
+        if keep:
+            out.append(line)
+    return "\n".join(out) + "\n"
+
+
 def main():
     ref = Reference()
     out = {}
@@ -66,6 +79,15 @@ def main():
     path = os.path.join(here, "golden.npz")
     np.savez_compressed(path, **out)
     print(path, sum(a.nbytes for a in out.values()), "bytes raw")
+    # The reference's acceptance harness on the reference library: criteria
+    # 1-7 are deterministic (criterion 8 needs the absent CLI and times).
+    acc = os.path.join(ROOT, "oracle", "_ref", "acceptance_reference")
+    if os.path.exists(acc):
+        import subprocess
+
+        txt = subprocess.run([acc], capture_output=True, text=True, timeout=1200).stdout
+        with open(os.path.join(here, "acceptance_reference.txt"), "w") as f:
+            f.write(acceptance_criteria(txt, range(1, 8)))
     # F4 formats: the reference's own FBEMAT01 store files and text mesh files
     for name, (op, dim, n, jit, bs, ce, prec) in FILES.items():
         ref.write_files(op, dim, n, jit, 42, bs, ce, prec, os.path.join(here, f"{name}.fbemat"),
