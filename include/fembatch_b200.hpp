@@ -116,6 +116,25 @@ AnalyticTensor build_k_elasticity(int dim);
 AnalyticTensor build_k_weighted_laplacian(int dim);
 AnalyticTensor build_analytic_tensor(Operator op, int dim);
 
+// Exact reference-cell quadrature of a product of P1 basis values and
+// first derivatives (the building block of K).  Result: one basis index per
+// slot (slot order), then one direction index per gradient factor (factor
+// order), row-major.
+enum class JetPart { value, gradient };
+struct JetFactor {
+  int slot = 0;
+  JetPart part = JetPart::value;
+};
+struct JetProductTensor {
+  std::vector<int> extents;
+  std::vector<double> data;
+};
+JetProductTensor integrate_jet_product(const TabulatedBasis& basis, const QuadratureRule& rule,
+                                       std::span<const JetFactor> factors);
+// Plain-text dump of K: "# <op> dim=.. krows=.. coefficient_blocks=.." and
+// one "block i=.. j=..[ k=..]" stanza per block, rows of 17 significant digits.
+void dump_analytic_tensor(std::ostream& os, const AnalyticTensor& k);
+
 // ---- geometry (reference include/fembatch/geometry.hpp) -------------------
 struct Mesh {
   int dim = 0;

@@ -4,6 +4,8 @@
 // src/kernel_config.cpp); the integration calls run on the GPU.
 #include "../../include/fembatch_b200.hpp"
 
+#include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <iomanip>
 #include <istream>
@@ -172,6 +174,82 @@ TabulatedBasis tabulate_p1_basis(const ReferenceCell& cell, const QuadratureRule
     t.values[q] = rest;
   }
   return t;
+}
+
+JetProductTensor integrate_jet_product(const TabulatedBasis& basis, const QuadratureRule& rule,
+                                       std::span<const JetFactor> factors)
+{
+  if (factors.empty())
+    throw std::invalid_argument("jet product needs at least one factor");
+  if (basis.dim != rule.dim || basis.num_points != rule.num_points())
+    throw std::invalid_argument("basis was tabulated for a different rule");
+  int slots = 0, values = 0;
+  for (const JetFactor& f : factors)
+  {
+    if (f.slot < 0)
+      throw std::invalid_argument("negative basis slot");
+    slots = std::max(slots, f.slot + 1);
+    values += f.part == JetPart::value ? 1 : 0;  // P1: values degree 1, derivatives degree 0
+  }
+  for (int sl = 0; sl < slots; ++sl)
+    if (std::none_of(factors.begin(), factors.end(), [&](const JetFactor& f) { return f.slot == sl; }))
+      throw std::invalid_argument("factor slots must cover 0..S-1");
+  if (rule.degree < values)
+    throw std::invalid_argument("quadrature degree " + std::to_string(rule.degree)
+                                + " insufficient for integrand degree " + std::to_string(values));
+  JetProductTensor t;
+  t.extents.assign(slots, basis.num_basis_funcs);
+  for (const JetFactor& f : factors)
+    if (f.part == JetPart::gradient)
+      t.extents.push_back(basis.dim);
+  std::int64_t n = 1;
+  for (int e : t.extents)
+    n *= e;
+  t.data.assign(static_cast<std::size_t>(n), 0.0);
+  std::vector<int> idx(t.extents.size(), 0);  // odometer over the result, last index fastest
+  for (std::int64_t flat = 0; flat < n; ++flat)
+  {
+    double acc = 0.0;
+    for (int q = 0; q < rule.num_points(); ++q)
+    {
+      double prod = 1.0;
+      int d = slots;  // next direction index
+      for (const JetFactor& f : factors)
+        prod *= f.part == JetPart::value ? basis.value(idx[f.slot], q) : basis.gradient(idx[f.slot], q, idx[d++]);
+      acc += rule.weights[q] * prod;
+    }
+    t.data[static_cast<std::size_t>(flat)] = acc;
+    for (int k = static_cast<int>(idx.size()) - 1; k >= 0 && ++idx[k] == t.extents[k]; --k)
+      idx[k] = 0;
+  }
+  return t;
+}
+
+void dump_analytic_tensor(std::ostream& os, const AnalyticTensor& k)
+{
+  const FormSpec& sp = k.spec;
+  os << "# " << operator_name(sp.op) << " dim=" << sp.dim << " krows=" << sp.krows()
+     << " coefficient_blocks=" << sp.num_coefficient_blocks() << "\n";
+  char buf[64];
+  for (int i = 0; i < sp.krows(); ++i)
+    for (int j = 0; j < sp.krows(); ++j)
+      for (int c = 0; c < sp.num_coefficient_blocks(); ++c)
+      {
+        os << "block i=" << i << " j=" << j;
+        if (sp.coefficient_arity > 0)
+          os << " k=" << c;
+        os << "\n";
+        for (int mu = 0; mu < sp.dim; ++mu)
+        {
+          for (int nu = 0; nu < sp.dim; ++nu)
+          {
+            std::snprintf(buf, sizeof buf, "%s%.17g", nu == 0 ? "" : " ", k.entry(i, j, c, mu, nu));
+            os << buf;
+          }
+          os << "\n";
+        }
+        os << "\n";
+      }
 }
 
 // -------------------------------------------------------------------- forms
