@@ -85,9 +85,14 @@ def main():
     if os.path.exists(acc):
         import subprocess
 
-        txt = subprocess.run([acc], capture_output=True, text=True, timeout=1200).stdout
+        cli = os.path.join(ROOT, "oracle", "_ref", "fembatch_cli_reference")
+        txt = subprocess.run([acc] + ([cli] if os.path.exists(cli) else []), capture_output=True, text=True,
+                             timeout=1200).stdout
         with open(os.path.join(here, "acceptance_reference.txt"), "w") as f:
             f.write(acceptance_criteria(txt, range(1, 8)))
+        with open(os.path.join(here, "acceptance_reference_verdicts.txt"), "w") as f:
+            f.write("".join(line + "\n" for line in txt.splitlines()
+                            if line.startswith(("[PASS] criterion", "[FAIL] criterion"))))
     # F4 formats: the reference's own FBEMAT01 store files and text mesh files
     for name, (op, dim, n, jit, bs, ce, prec) in FILES.items():
         ref.write_files(op, dim, n, jit, 42, bs, ce, prec, os.path.join(here, f"{name}.fbemat"),
