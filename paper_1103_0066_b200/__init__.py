@@ -30,5 +30,6 @@ from .engine import (  # noqa: F401
 )
 from .assembly import AssemblyPlan, assemble, assembly_plan  # noqa: F401
 from .mesh import jitter_mesh, mesh_prefix, structured_mesh  # noqa: F401
+from .storeio import read_mesh_text, read_store, write_mesh_text, write_store  # noqa: F401
 
 __version__ = "0.1.0"

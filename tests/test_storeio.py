@@ -1,0 +1,56 @@
+"""F4 formats from Python (paper_1103_0066_b200/storeio.py) against files the
+unmodified reference wrote (tests/golden/*.fbemat, *.mesh; make_golden.py):
+byte-exact re-writes, the reference's stored matrices equal to the oracle
+restatement's for the reference's mesh file, and (GPU) the engine's store of
+that mesh written as the reference's file byte for byte."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1103_0066_b200 as fb
+from paper_1103_0066_b200 import storeio
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+FILES = {"ref_store_2d_elasticity_f32": ("elasticity", 8, 2, "f32"),
+         "ref_store_3d_laplacian_f64": ("laplacian", 16, 1, "f64")}
+
+
+@pytest.mark.parametrize("name", sorted(FILES))
+def test_reference_files_round_trip_byte_exact(tmp_path, name, restatement):
+    op, bs, ce, prec = FILES[name]
+    sf = storeio.read_store(os.path.join(GOLDEN, name + ".fbemat"))
+    assert (sf.element_batch_size, sf.num_concurrent_elements) == (bs, ce)
+    assert sf.data.dtype == (np.float32 if prec == "f32" else np.float64)
+    out = tmp_path / "s.fbemat"
+    storeio.write_store(str(out), sf.data, sf.dim, sf.krows, bs, sf.num_elements, ce)
+    assert out.read_bytes() == open(os.path.join(GOLDEN, name + ".fbemat"), "rb").read()
+    dim, v, c = storeio.read_mesh_text(os.path.join(GOLDEN, name + ".mesh"))
+    m = tmp_path / "m.mesh"
+    storeio.write_mesh_text(str(m), v, c, dim)
+    assert m.read_text() == open(os.path.join(GOLDEN, name + ".mesh")).read()
+    # the reference's stored matrices == the oracle restatement on the reference's mesh
+    want = restatement.integrate_mesh(op, v, c, dim, bs=bs, precision=prec)
+    assert sf.data.tobytes() == want.tobytes()
+
+
+def test_store_validation(tmp_path):
+    bad = tmp_path / "bad.fbemat"
+    bad.write_bytes(b"NOTASTORE")
+    with pytest.raises(ValueError, match="not an element-matrix store"):
+        storeio.read_store(str(bad))
+    with pytest.raises(ValueError, match="length"):
+        storeio.write_store(str(bad), np.zeros(5, np.float32), 2, 3, 4, 5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(FILES))
+def test_gpu_store_written_equals_reference_file(tmp_path, name):
+    op, bs, ce, prec = FILES[name]
+    dim, v, c = storeio.read_mesh_text(os.path.join(GOLDEN, name + ".mesh"))
+    var = fb.make_variant(op, dim, prec, "strict", element_batch_size=bs, num_concurrent_elements=ce,
+                          interleave_stores=True)
+    store = fb.integrate_mesh(var, v, c)
+    out = tmp_path / "s.fbemat"
+    storeio.write_store(str(out), store, dim, var.spec.krows, bs, c.size // (dim + 1), ce)
+    assert out.read_bytes() == open(os.path.join(GOLDEN, name + ".fbemat"), "rb").read()
