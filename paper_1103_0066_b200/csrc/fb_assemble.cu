@@ -270,31 +270,10 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
       else
         load_plan(q + 32 * U, pk, ps);
     }
-    if constexpr (NCW == NC)
-    {
-      // Each lane's finished row (segment) is contiguous: row + slot for
-      // slot < deg*NC.  Write the 32 segments one after another with the
-      // whole warp (coalesced 128-byte lines) instead of each lane storing
-      // its own scattered segment (one L1 wavefront per lane per store).
-      const int len = in_smem ? deg * NC : 0;  // out-of-smem rows were written in place
-      __syncwarp();
-      const int wbase = threadIdx.x - lane;
-#pragma unroll 1
-      for (int j = 0; j < 32; ++j)
-      {
-        const int lj = __shfl_sync(0xffffffffu, len, j);
-        const long long sj = __shfl_sync(0xffffffffu, static_cast<long long>(row), j);
-        for (int t = lane; t < lj; t += 32)
-          vals[sj + t] = acc_s[t * T + wbase + j];
-      }
-      __syncwarp();
-    }
-    else if (in_smem)
-    {
+    if (in_smem)
       for (int k = 0; k < deg; ++k)
         for (int c = 0; c < NCW; ++c)
           vals[row + k * NC + c] = acc[(k * NCW + c) * T];
-    }
     cur = nxt;
   }
 }
