@@ -37,7 +37,7 @@ unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std:
 // swizzle = the row size (64 / 128 bytes).  False if the driver entry point is
 // unavailable or the encoding is rejected (the caller then uses the LDS/STG
 // copy).
-bool encode_store_map(CUtensorMap* tm, void* out, int64_t rows, int row_scalars, int scalar_bytes);
+bool encode_store_map(CUtensorMap* tm, void* out, int64_t rows, int row_scalars, int scalar_bytes, int box_rows);
 
 template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G, int ST>
 cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st)
@@ -47,7 +47,7 @@ cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st
   CUtensorMap tm{};
   if constexpr (ST == kStTma && WS::TMA == 2)
   {
-    if (!encode_store_map(&tm, a.out, a.nloc, WS::NK, (int)sizeof(S)))
+    if (!encode_store_map(&tm, a.out, a.nloc, WS::NK, (int)sizeof(S), 32 * WS::TG))
       return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStCopy>(a, kb, st);
   }
   auto kernel = fb_integrate_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, ST>;

@@ -42,7 +42,7 @@ EncodeFn encoder()
 }
 }  // namespace
 
-bool encode_store_map(CUtensorMap* tm, void* out, int64_t rows, int row_scalars, int scalar_bytes)
+bool encode_store_map(CUtensorMap* tm, void* out, int64_t rows, int row_scalars, int scalar_bytes, int box_rows)
 {
   const int row_bytes = row_scalars * scalar_bytes;
   if (row_bytes != 64 && row_bytes != 128)
@@ -54,7 +54,9 @@ bool encode_store_map(CUtensorMap* tm, void* out, int64_t rows, int row_scalars,
     return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_scalars), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_bytes)};  // bytes, dims 1..rank-1
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(row_scalars), 32};
+  if (box_rows < 1 || box_rows > 256)
+    return false;
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(row_scalars), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r =
       f(tm, scalar_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims,
