@@ -171,7 +171,7 @@ def test_nonsymmetric_k_takes_sparse_path(restatement):
 @pytest.mark.parametrize("dim", [2, 3])
 def test_ragged_sizes_and_padding(restatement, ne, dim):
     v, c, _ = fb.mesh_prefix(dim, ne, 0.1, 11)
-    for prec, op in (("f32", "laplacian"), ("f64", "elasticity")):
+    for prec, op in (("f32", "laplacian"), ("f64", "elasticity"), ("f32", "elasticity"), ("f64", "laplacian")):
         for bs in (1, 7, 128):
             var = fb.make_variant(op, dim, prec, element_batch_size=bs)
             got = fb.integrate_mesh(var, v, c)
