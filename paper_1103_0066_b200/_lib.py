@@ -33,7 +33,7 @@ class fb_error(C.Structure):
 
 
 # name -> (restype, argtypes); every symbol declared in include/fembatch_b200.h
-_i32, _i64, _vp, _dp = C.c_int, C.c_int64, C.c_void_p, C.c_void_p
+_i32, _i64, _vp = C.c_int, C.c_int64, C.c_void_p
 _E = C.POINTER(fb_error)
 SIGNATURES = {
     "fb_abi_version": (_i32, []),

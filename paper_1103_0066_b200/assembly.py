@@ -11,7 +11,6 @@ result is bitwise the serial element-order sum.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Optional
 
 import numpy as np
 

@@ -11,7 +11,7 @@ C ABI into sm_100a kernels; arrays may be numpy (host) or torch CUDA tensors
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import numpy as np

@@ -2,7 +2,6 @@
 header declares, its pure host functions reproduce the reference's goldens,
 specialization validates like the reference (same exception texts), and the
 integration entry points fail loudly -- never fall back -- without a GPU."""
-import ctypes as C
 import os
 import re
 
