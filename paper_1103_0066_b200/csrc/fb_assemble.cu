@@ -39,9 +39,6 @@ namespace {
 // in shared memory (<= 48 KB static per CTA); vertices with more neighbours
 // accumulate in their own rows of the output.  U = incidences in flight per
 // lane.
-#ifndef FB_ASM_COALESCE
-#define FB_ASM_COALESCE 1  // scalar forms: staged, coalesced write-out of the warp's rows
-#endif
 #ifndef FB_ASM_NCW2
 #define FB_ASM_NCW2 2  // 2D elasticity: a warp reads the whole element row (A/B: 1 is slower)
 #endif
@@ -52,7 +49,7 @@ template <class S, int DIM, int NC>
 struct AsmShape {
   static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : 1);
   static constexpr int WARPS = NCW == 1 ? 4 : 2;
-  static constexpr int SLOTS = (NCW == 1 && !(NC == 1 && FB_ASM_COALESCE && sizeof(S) == 8)) ? 32 : 24;
+  static constexpr int SLOTS = NCW == 1 ? 32 : 24;
   static constexpr int U = DIM == 2 ? FB_ASM_U2D : (NCW == 1 ? FB_ASM_U : 4);
   // prefetch the next chunk's plan entries (registers: 3D elasticity FP64,
   // already at the register limit, is faster without -- A/B measured)
@@ -60,8 +57,7 @@ struct AsmShape {
   // batch the slot updates of one incidence (all loads, adds, stores): faster
   // in FP32, slower in FP64 (register pressure) -- A/B measured
   static constexpr bool BATCH = sizeof(S) == 4;
-  static_assert(SLOTS * NCW * 32 * WARPS * sizeof(S) * ((NC == 1 && FB_ASM_COALESCE) ? 2 : 1) <= 48 * 1024,
-                "static smem");
+  static_assert(SLOTS * NCW * 32 * WARPS * sizeof(S) <= 48 * 1024, "static smem");
 };
 constexpr uint32_t kPad = 0xffffffffu;
 
@@ -140,8 +136,6 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   constexpr int SLOTS = Sh::SLOTS;
   constexpr int U = Sh::U;
   __shared__ S acc_s[SLOTS * NCW * T];
-  // coalesced write-out staging (scalar forms): 32 rows of <= SLOTS values per warp
-  __shared__ S stage_s[(NC == 1 && FB_ASM_COALESCE) ? 32 * SLOTS * (T / 32) : 1];
   S* acc = acc_s + threadIdx.x;
   S* vals = static_cast<S*>(a.values);
   const S* store = static_cast<const S*>(a.store);
@@ -276,40 +270,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
       else
         load_plan(q + 32 * U, pk, ps);
     }
-    if constexpr (NC == 1 && FB_ASM_COALESCE)
-    {
-      // Scalar forms: the warp's 32 rows are one contiguous range of the
-      // values (row blocks of consecutive vertices).  Each lane copies its
-      // row into a warp-private staging buffer at its exclusive-scan offset,
-      // then the warp streams the range out with coalesced stores -- instead
-      // of 32 scattered per-lane row stores.  A warp with an out-of-smem row
-      // (written in place) keeps the per-lane path.
-      const bool all_smem = __all_sync(0xffffffffu, in_smem);
-      if (all_smem)
-      {
-        int incl = deg;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1)
-        {
-          const int y = __shfl_up_sync(0xffffffffu, incl, d);
-          incl += lane >= d ? y : 0;
-        }
-        const int off = incl - deg;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const long long g0 = __shfl_sync(0xffffffffu, static_cast<long long>(row), 0);
-        S* stg = stage_s + (threadIdx.x >> 5) * (32 * SLOTS);
-        for (int k = 0; k < deg; ++k)
-          stg[off + k] = acc[k * T];
-        __syncwarp();
-        for (int q = lane; q < total; q += 32)
-          vals[g0 + q] = stg[q];
-        __syncwarp();
-      }
-      else if (in_smem)
-        for (int k = 0; k < deg; ++k)
-          vals[row + k] = acc[k * T];
-    }
-    else if (in_smem)
+    if (in_smem)
       for (int k = 0; k < deg; ++k)
         for (int c = 0; c < NCW; ++c)
           vals[row + k * NC + c] = acc[(k * NCW + c) * T];
