@@ -22,6 +22,11 @@ unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std:
   {
     int blocks = 0, dev = 0, sms = 0;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#ifdef FB_CARVEOUT
+    // A/B: preferred shared-memory carveout (percent of the maximum); the
+    // rest of the 256 KB per SM is L1 for the coordinate gathers
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, FB_CARVEOUT);
+#endif
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
