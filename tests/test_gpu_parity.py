@@ -343,6 +343,36 @@ def test_multi_device_with_device_resident_buffers(restatement):
     assert hout.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("dim,n", [(2, 9), (3, 4)])
+def test_unaligned_inputs_take_the_scalar_load_paths(restatement, dim, n):
+    """Vertex / connectivity arrays that are not 16-byte aligned (2D: no
+    double2 vertex loads; 3D: no int4 connectivity loads) give the same bits."""
+    import torch
+
+    v, c = mesh(dim, n)
+    ne = c.size // (dim + 1)
+    vb = torch.empty(v.size + 1, dtype=torch.float64, device="cuda")
+    cb = torch.empty(c.size + 1, dtype=torch.int32, device="cuda")
+    vb[1:] = torch.from_numpy(v)
+    cb[1:] = torch.from_numpy(c)
+    st = torch.empty(2, dtype=torch.int64, device="cuda")
+    sid = torch.cuda.current_stream().cuda_stream
+    for op, prec in (("laplacian", "f64"), ("elasticity", "f32")):
+        var = fb.make_variant(op, dim, prec, "strict", element_batch_size=16)
+        want = restatement.integrate_mesh(op, v, c, dim, bs=16, precision=prec)
+        out = torch.empty(want.size, dtype=torch.float32 if prec == "f32" else torch.float64, device="cuda")
+        fb.status_reset(st, sid)
+        fb.integrate_mesh_async(var, vb[1:], cb[1:], out, st, sid)
+        fb.status_check(st, sid)
+        assert out.cpu().numpy().tobytes() == want.tobytes()
+        gw = restatement.pack_geometry(v, c, dim, 16, prec)
+        g = torch.empty(gw.size, dtype=out.dtype, device="cuda")
+        fb.pack_geometry_async(vb[1:], cb[1:], dim, g, st, 16, prec, sid)
+        fb.status_check(st, sid)
+        assert g.cpu().numpy().tobytes() == gw.tobytes()
+    assert ne > 0
+
+
 def test_async_api_is_cuda_graph_capturable(restatement):
     """The device-resident entry points enqueue kernels only (no allocation,
     no synchronisation), so a whole mesh -> matrices -> CSR pipeline can be
