@@ -167,6 +167,21 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   Desc cur;
   if (w < nwarps)
     cur = load_desc(w);
+  // plan entries of the chunk about to be processed; pk_task = the task they
+  // belong to (the next task's first chunk is prefetched during the current
+  // task's last chunk)
+  uint32_t pk[U], ps[U];
+  int64_t pk_task = -1;
+  auto load_plan = [&](int64_t q, int64_t qend, uint32_t (&k)[U], uint32_t (&p)[U])
+  {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+    {
+      const int64_t qu = q + 32 * u;
+      k[u] = qu < qend ? __ldg(a.spk + qu) : kPad;
+      p[u] = qu < qend ? __ldg(a.spos + qu) : 0u;
+    }
+  };
   for (; w < nwarps; w += wstride)
   {
     Desc nxt;
@@ -183,18 +198,8 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
     const bool in_smem = deg <= SLOTS;
     // the plan entries of chunk i+1 are loaded while chunk i's element rows
     // are gathered and added (one exposed latency per chunk, not two)
-    uint32_t pk[U], ps[U];
-    auto load_plan = [&](int64_t q, uint32_t (&k)[U], uint32_t (&p)[U])
-    {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-      {
-        const int64_t qu = q + 32 * u;
-        k[u] = qu < q1 ? __ldg(a.spk + qu) : kPad;
-        p[u] = qu < q1 ? __ldg(a.spos + qu) : 0u;
-      }
-    };
-    load_plan(q0 + lane, pk, ps);
+    if (pk_task != w)
+      load_plan(q0 + lane, q1, pk, ps);
     // zero the accumulators while the plan entries are in flight
     if (in_smem)
       for (int k = 0; k < deg * NCW; ++k)
@@ -206,8 +211,19 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
       uint32_t npk[U], nps[U];
+      int64_t npk_task = w;
       if constexpr (Sh::PREF)
-        load_plan(q + 32 * U, npk, nps);
+      {
+        if (q + 32 * U < q1)
+          load_plan(q + 32 * U, q1, npk, nps);
+        else if (w + wstride < nwarps)
+        {
+          load_plan(nxt.q0 + lane, nxt.q1, npk, nps);  // the next task's first chunk
+          npk_task = w + wstride;
+        }
+        else
+          npk_task = -1;
+      }
       S r[U][NB * NCW];
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -266,9 +282,13 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
           pk[u] = npk[u];
           ps[u] = nps[u];
         }
+        pk_task = npk_task;
       }
       else
-        load_plan(q + 32 * U, pk, ps);
+      {
+        load_plan(q + 32 * U, q1, pk, ps);
+        pk_task = q + 32 * U < q1 ? w : -1;
+      }
     }
     if (in_smem)
       for (int k = 0; k < deg; ++k)
