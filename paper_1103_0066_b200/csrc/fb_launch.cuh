@@ -34,7 +34,12 @@ unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std:
     per = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
     slots.store(per, std::memory_order_relaxed);
   }
+#ifdef FB_NONPERSIST  // A/B: one warp tile per warp, the hardware schedules the CTAs
+  (void)per;
+  return (unsigned)nctas;
+#else
   return (unsigned)(nctas < per ? nctas : per);
+#endif
 }
 
 // Tensor map of a launch's store viewed as rows of one element matrix
