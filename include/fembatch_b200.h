@@ -190,6 +190,13 @@ int fb_pack_geometry(const fb_mesh_view* mesh, int element_batch_size,
                      int precision, void* g_out, int64_t g_len,
                      const int* devices, int ndev, fb_error* err);
 
+/* ---- device buffers (for callers without their own allocator) ------------
+ * fb_device_alloc: `bytes` of device memory on `device` (256-byte aligned,
+ * so staged/TMA stores apply), NULL on failure (err filled).  fb_free
+ * releases it (NULL is a no-op). */
+void* fb_device_alloc(int64_t bytes, int device, fb_error* err);
+int fb_free(void* device_ptr, fb_error* err);
+
 /* ---- device-resident asynchronous API ------------------------------------
  * All pointers are device pointers on the current device; the launch is
  * enqueued on `stream` (a cudaStream_t, NULL = legacy default stream) and the

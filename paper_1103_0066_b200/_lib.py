@@ -57,6 +57,8 @@ SIGNATURES = {
     "fb_pack_geometry": (_i32, [C.POINTER(fb_mesh_view), _i32, _i32, _vp, _i64, _vp, _i32, _E]),
     "fb_integrate_mesh_async": (_i32, [_vp, C.POINTER(fb_mesh_view), _vp, _vp, _i64, _vp, _vp, _E]),
     "fb_integrate_packed_async": (_i32, [_vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _E]),
+    "fb_device_alloc": (_vp, [_i64, _i32, _E]),
+    "fb_free": (_i32, [_vp, _E]),
     "fb_pack_geometry_async": (_i32, [C.POINTER(fb_mesh_view), _i32, _i32, _vp, _i64, _vp, _vp, _E]),
     "fb_status_reset": (_i32, [_vp, _vp, _E]),
     "fb_status_check": (_i32, [_vp, _vp, _E]),

@@ -805,6 +805,38 @@ int fb_pack_geometry(const fb_mesh_view* mesh, int bs, int precision, void* g_ou
                  });
 }
 
+void* fb_device_alloc(int64_t bytes, int device, fb_error* err)
+{
+  void* p = nullptr;
+  guarded(err,
+          [&]
+          {
+            if (bytes < 0)
+              invalid("negative allocation size");
+            if (device_count() == 0)
+              throw_code(FB_ERR_NO_DEVICE, "no CUDA device available");
+            if (device < 0 || device >= device_count())
+              invalid("device " + std::to_string(device) + " does not exist");
+            int cur = 0;
+            cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+            cuda_check(cudaSetDevice(device), "cudaSetDevice");
+            const cudaError_t e = cudaMalloc(&p, std::max<int64_t>(bytes, 1));
+            cudaSetDevice(cur);
+            cuda_check(e, "cudaMalloc");
+          });
+  return p;
+}
+
+int fb_free(void* device_ptr, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   if (device_ptr)
+                     cuda_check(cudaFree(device_ptr), "cudaFree");
+                 });
+}
+
 int fb_pack_geometry_async(const fb_mesh_view* mesh, int bs, int precision, void* g_out, int64_t g_len,
                            int64_t* status, void* stream, fb_error* err)
 {

@@ -137,3 +137,14 @@ def test_validation_precedes_device_use():
     out = np.zeros(5)
     with pytest.raises(ValueError, match="output buffer holds 5 scalars"):
         fb.integrate_mesh(lap, v, c, out=out)
+
+
+def test_device_alloc_without_a_gpu_fails_loudly():
+    import ctypes
+
+    lib = _lib.load()
+    err = _lib.fb_error()
+    if lib.fb_device_count() == 0:
+        assert lib.fb_device_alloc(1024, 0, ctypes.byref(err)) is None
+        assert err.code == _lib.FB_ERR_NO_DEVICE
+    assert lib.fb_free(None, ctypes.byref(err)) == _lib.FB_OK

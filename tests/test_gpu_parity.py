@@ -8,6 +8,8 @@ Bar:
   <= 1e-13 (f64) and <= 5e-6 (f32);
 * connectivity / indexing / padding: exact.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -406,6 +408,40 @@ def test_async_api_is_cuda_graph_capturable(restatement):
     assert out.cpu().numpy().tobytes() == want.tobytes()
     rp, ci = plan.pattern()
     assert vals.cpu().numpy().tobytes() == restatement.assemble("laplacian", 3, c, nv, "f32", want, rp, ci).tobytes()
+
+
+def test_library_allocated_device_store(restatement):
+    """fb_device_alloc / fb_free: a library-allocated device store used as the
+    output of the async entry point (read back with the CUDA runtime)."""
+    import ctypes
+    import glob
+
+    import nvidia.cuda_runtime
+    import torch
+
+    cudart = ctypes.CDLL(glob.glob(os.path.join(list(nvidia.cuda_runtime.__path__)[0], "lib", "libcudart.so*"))[0])
+    lib = fb.engine.L.load()
+    v, c = mesh(2, 6)
+    ne = c.size // 3
+    var = fb.make_variant("elasticity", 2, "f64", "strict", element_batch_size=8)
+    n = var.store_length(ne)
+    err = fb.engine.L.fb_error()
+    p = lib.fb_device_alloc(n * 8, 0, ctypes.byref(err))
+    assert p and p % 256 == 0
+    st = torch.empty(2, dtype=torch.int64, device="cuda")
+    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+    mv = fb.engine.mesh_view(dv, dc, 2)
+    sid = torch.cuda.current_stream().cuda_stream
+    fb.status_reset(st, sid)
+    rc = lib.fb_integrate_mesh_async(var.handle, ctypes.byref(mv), None, ctypes.c_void_p(p), n, st.data_ptr(),
+                                     ctypes.c_void_p(sid), ctypes.byref(err))
+    assert rc == 0, err.message
+    fb.status_check(st, sid)
+    host = np.empty(n, dtype=np.float64)
+    assert cudart.cudaMemcpy(ctypes.c_void_p(host.ctypes.data), ctypes.c_void_p(p), ctypes.c_size_t(n * 8), 2) == 0
+    want = restatement.integrate_mesh("elasticity", v, c, 2, bs=8, precision="f64")
+    assert host.tobytes() == want.tobytes()
+    assert lib.fb_free(ctypes.c_void_p(p), ctypes.byref(err)) == 0
 
 
 def test_launch_counter_counts_kernels():
