@@ -262,6 +262,17 @@ int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, in
 int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* store,
                       int64_t store_len, void* values, int64_t nnz, int flags, void* stream,
                       fb_error* err);
+/* Assembly straight from packed geometry (the fb_integrate_batches input:
+ * g = num_elements*dim^2 scalars in engine precision, PackedGeometry layout;
+ * coeffs = num_elements*(dim+1) doubles for the weighted Laplacian, else
+ * NULL): each incidence's element-matrix row is recomputed in registers, the
+ * element-matrix store is never written.  values are bitwise those of
+ * fb_integrate_batches(g) followed by fb_assemble.  Needs a variant whose K
+ * has the P1 pattern (fb_variant_path != 2).  Device pointers on the current
+ * device; enqueued on `stream`. */
+int fb_assemble_packed_async(const fb_assembly* a, const fb_variant* v, const void* g, int64_t g_len,
+                             const double* coeffs, int64_t coeffs_len, void* values, int64_t nnz,
+                             void* stream, fb_error* err);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,7 @@ SIGNATURES = {
     "fb_assembly_pattern": (_i32, [_vp, _vp, _i64, _vp, _i64, _E]),
     "fb_assemble": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _E]),
     "fb_assemble_async": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _E]),
+    "fb_assemble_packed_async": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _E]),
 }
 
 _lib = None

@@ -92,6 +92,18 @@ class AssemblyPlan:
                                          C.c_void_p(stream), C.byref(err))
         L.raise_for(rc, err)
 
+    def assemble_packed_async(self, variant: KernelVariant, g, values, coeffs=None, stream: int = 0):
+        """Enqueue assembly straight from packed geometry ``g`` (the
+        ``integrate_batches`` input, device tensor in engine precision): the
+        element matrices are recomputed per incidence and never stored.
+        Bitwise ``assemble(integrate_batches(g))``.  Device tensors only."""
+        err = L.fb_error()
+        rc = self._lib.fb_assemble_packed_async(self._h, variant.handle, _ptr(g), _numel(g),
+                                                _ptr(coeffs) if coeffs is not None else None,
+                                                _numel(coeffs) if coeffs is not None else 0,
+                                                _ptr(values), _numel(values), C.c_void_p(stream), C.byref(err))
+        L.raise_for(rc, err)
+
 
 def assembly_plan(op: str, dim: int, cells, num_vertices: int) -> AssemblyPlan:
     return AssemblyPlan(op, dim, cells, num_vertices)

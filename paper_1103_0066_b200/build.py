@@ -31,6 +31,7 @@ CU_SOURCES = [
     "fb_pack.cu",
     "fb_assemble.cu",
     "fb_plan.cu",
+    "fb_assemble_g.cu",
 ]
 CPP_SOURCES = ["fb_capi.cpp", "fb_assembly.cpp", "fb_host.cpp", "fembatch_api.cpp"]
 CU_HOST_SOURCES = ["fb_tma.cpp"]  # host code that includes the kernel headers (nvcc)

@@ -1,0 +1,226 @@
+// fb_assemble_g.cu -- global CSR assembly straight from the packed geometry
+// (G, reference PackedGeometry layout): the element matrices are never
+// stored.  Same plan, same deterministic per-vertex gather as fb_assemble.cu,
+// but each incidence's element-matrix row is recomputed in registers from
+// G_e with the G-input integration path's own contraction (contract_sparse,
+// fb_kernels.cuh; same arithmetic mode, no symmetric shortcut), so every
+// contribution has the bits integrate_batches would have stored and the sum
+// order is the same ascending element order: the values are bitwise those of
+// assembling the integrate_batches store.  For elasticity only the c_i == c_j
+// component blocks are added (the others are +0, an identity for an
+// accumulator that starts at +0 and is never -0).
+//
+// Bytes per element: G (dim^2 scalars) read once per incidence instead of an
+// element-matrix row, and no store written -- the win grows with krows^2
+// (3D elasticity: 36 B of G vs a 576 B matrix).
+#include <atomic>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "fb_kernels.cuh"
+
+namespace fbk {
+
+std::atomic<long long>& launch_counter();
+
+namespace {
+
+constexpr uint32_t kPadG = 0xffffffffu;
+
+template <class S>
+__device__ __forceinline__ S add_rn_g(S a, S b);
+template <>
+__device__ __forceinline__ float add_rn_g(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn_g(double a, double b) { return __dadd_rn(a, b); }
+
+template <class S, int DIM, int OP>
+struct GShape {
+  static constexpr int NC = OP == kElasticity ? DIM : 1;
+  static constexpr int WARPS = 4;
+  // neighbours x components accumulated in shared memory (<= 48 KB static)
+  static constexpr int FIT = 48 * 1024 / (NC * 32 * WARPS * static_cast<int>(sizeof(S)));
+  static constexpr int SLOTS = FIT < 32 ? FIT : 32;
+  static constexpr int U = 4;  // incidences in flight per lane
+};
+
+// Row aa (runtime) of the nb x nb Laplacian-like block, selected without
+// dynamic register indexing.
+template <class S, int NB>
+__device__ __forceinline__ void select_row(const S (&vv)[NB * NB], int aa, S (&x)[NB])
+{
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+    x[b] = vv[b];
+#pragma unroll
+  for (int r = 1; r < NB; ++r)
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      x[b] = aa == r ? vv[r * NB + b] : x[b];
+}
+
+// A warp owns 32 consecutive vertices and all their rows.  Elasticity: the
+// element matrix is block diagonal with nc copies of the Laplacian-like
+// block, so each incidence's row is computed once and added to the nc
+// diagonal component blocks; the off-diagonal blocks are written as +0.
+template <class S, int DIM, int OP, int MODE, bool UNI>
+__global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
+    fb_assemble_g_kernel(const AsmArgs a, const KP<S, DIM, OP> kp)
+{
+  using G = GShape<S, DIM, OP>;
+  constexpr int NB = DIM + 1, NC = G::NC, DD = DIM * DIM;
+  constexpr int T = 32 * G::WARPS, SLOTS = G::SLOTS, U = G::U;
+  __shared__ S acc_s[SLOTS * NC * T];
+  S* acc = acc_s + threadIdx.x;
+  S* vals = static_cast<S*>(a.values);
+  const S* gin = static_cast<const S*>(a.g_in);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (a.nv + 31) / 32;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); g < nwarps;
+       g += static_cast<int64_t>(gridDim.x) * (T / 32))
+  {
+    const int64_t v = g * 32 + lane;
+    const bool live = v < a.nv;
+    const int64_t r0 = live ? __ldg(a.nbr_ptr + v) : 0;
+    const int deg = live ? static_cast<int>(__ldg(a.nbr_ptr + v + 1) - r0) : 0;
+    // CSR row (v, ci) starts at r0*NC*NC + ci*deg*NC; entry (k, cj) at + k*NC + cj.
+    // Diagonal-block accumulator (k, ci) -> acc slot k*NC + ci.
+    const int64_t row0 = r0 * NC * NC;
+    const bool in_smem = deg <= SLOTS;
+    const int64_t q0 = __ldg(a.goff + g), q1 = __ldg(a.goff + g + 1);
+    uint32_t pk[U], ps[U];
+    auto load_plan = [&](int64_t q, uint32_t (&k)[U], uint32_t (&p)[U])
+    {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+      {
+        const int64_t qu = q + 32 * u;
+        k[u] = qu < q1 ? __ldg(a.spk + qu) : kPadG;
+        p[u] = qu < q1 ? __ldg(a.spos + qu) : 0u;
+      }
+    };
+    load_plan(q0 + lane, pk, ps);
+    if (in_smem)
+      for (int k = 0; k < deg * NC; ++k)
+        acc[k * T] = S(0);
+    else
+      for (int k = 0; k < deg * NC * NC; ++k)
+        vals[row0 + k] = S(0);
+    for (int64_t q = q0 + lane; q < q1; q += 32 * U)
+    {
+      uint32_t npk[U], nps[U];
+      load_plan(q + 32 * U, npk, nps);
+      S ge[U][DD];
+      S we[U][DIM + 1];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+      {
+        const int64_t e = pk[u] != kPadG ? (pk[u] >> 2) : 0;
+#pragma unroll
+        for (int t = 0; t < DD; ++t)
+          ge[u][t] = pk[u] != kPadG ? __ldg(gin + e * DD + t) : S(0);
+#pragma unroll
+        for (int c = 0; c <= DIM; ++c)
+          we[u][c] = OP == kWeighted && pk[u] != kPadG ? static_cast<S>(__ldg(a.coeffs + e * (DIM + 1) + c)) : S(0);
+      }
+      // one incidence at a time: two incidences may share a neighbour
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (pk[u] != kPadG)
+        {
+          S vv[NB * NB], x[NB];
+          contract_sparse<S, DIM, OP, MODE, false, UNI>(ge[u], we[u], kp, vv);
+          select_row<S, NB>(vv, static_cast<int>(pk[u] & 3u), x);
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+          {
+            const int k = static_cast<int>((ps[u] >> (8 * b)) & 0xffu);
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+            {
+              if (in_smem)
+                acc[(k * NC + c) * T] = add_rn_g(acc[(k * NC + c) * T], x[b]);
+              else
+              {
+                S* p = vals + row0 + static_cast<int64_t>(c) * deg * NC + k * NC + c;
+                *p = add_rn_g(*p, x[b]);
+              }
+            }
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+      {
+        pk[u] = npk[u];
+        ps[u] = nps[u];
+      }
+    }
+    if (in_smem)
+      for (int ci = 0; ci < NC; ++ci)
+        for (int k = 0; k < deg; ++k)
+#pragma unroll
+          for (int cj = 0; cj < NC; ++cj)
+            vals[row0 + static_cast<int64_t>(ci) * deg * NC + k * NC + cj] = cj == ci ? acc[(k * NC + ci) * T] : S(0);
+  }
+}
+
+template <class S, int DIM, int OP, int MODE, bool UNI>
+cudaError_t go_g(const AsmArgs& a, const KParamBlob& kb, cudaStream_t st)
+{
+  using G = GShape<S, DIM, OP>;
+  constexpr int T = 32 * G::WARPS;
+  const int64_t nwarps = (a.nv + 31) / 32;
+  if (nwarps <= 0)
+    return cudaSuccess;
+  static int grid_cap = 0;
+  if (grid_cap == 0)
+  {
+    int blocks = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_g_kernel<S, DIM, OP, MODE, UNI>, T, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid_cap = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
+  }
+  const int64_t need = (nwarps + T / 32 - 1) / (T / 32);
+  const unsigned grid = static_cast<unsigned>(need < grid_cap ? need : grid_cap);
+  const KP<S, DIM, OP>& kp = *reinterpret_cast<const KP<S, DIM, OP>*>(kb.bytes);
+  fb_assemble_g_kernel<S, DIM, OP, MODE, UNI><<<grid, T, 0, st>>>(a, kp);
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <class S, int DIM, int OP>
+cudaError_t go_g_mode(const LaunchSpec& s, const AsmArgs& a, const KParamBlob& kb, cudaStream_t st)
+{
+  const bool uni = s.path == kUniformSym;
+  if (s.mode == kFast)
+    return uni ? go_g<S, DIM, OP, kFast, true>(a, kb, st) : go_g<S, DIM, OP, kFast, false>(a, kb, st);
+  return uni ? go_g<S, DIM, OP, kStrict, true>(a, kb, st) : go_g<S, DIM, OP, kStrict, false>(a, kb, st);
+}
+
+template <class S, int DIM>
+cudaError_t go_g_op(const LaunchSpec& s, const AsmArgs& a, const KParamBlob& kb, cudaStream_t st)
+{
+  switch (s.op)
+  {
+  case kLaplacian:
+    return go_g_mode<S, DIM, kLaplacian>(s, a, kb, st);
+  case kElasticity:
+    return go_g_mode<S, DIM, kElasticity>(s, a, kb, st);
+  default:
+    return go_g_mode<S, DIM, kWeighted>(s, a, kb, st);
+  }
+}
+
+}  // namespace
+
+// s.path must be a sparse path (the dense fallback has no G-input assembly)
+cudaError_t launch_assemble_g(const LaunchSpec& s, const AsmArgs& a, const KParamBlob& kb, cudaStream_t st)
+{
+  if (s.prec == 0)
+    return s.dim == 2 ? go_g_op<float, 2>(s, a, kb, st) : go_g_op<float, 3>(s, a, kb, st);
+  return s.dim == 2 ? go_g_op<double, 2>(s, a, kb, st) : go_g_op<double, 3>(s, a, kb, st);
+}
+
+}  // namespace fbk

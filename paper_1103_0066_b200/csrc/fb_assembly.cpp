@@ -418,6 +418,54 @@ int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* sto
                  });
 }
 
+int fb_assemble_packed_async(const fb_assembly* a, const fb_variant* v, const void* g, int64_t g_len,
+                             const double* coeffs, int64_t coeffs_len, void* values, int64_t nnz, void* stream,
+                             fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   check_pair(a, v, a ? a->ne * (v ? v->krows * v->krows : 0) : 0, nnz);
+                   const int64_t dd = static_cast<int64_t>(a->dim) * a->dim;
+                   if (v->path == fbk::kDense)
+                     invalid("packed-geometry assembly needs a K with the P1 sparsity pattern");
+                   if (a->ne > 0 && !g)
+                     invalid("null packed geometry");
+                   if (g_len < a->ne * dd)
+                     invalid("packed geometry shorter than num_elements * dim^2");
+                   if (v->op == FB_WEIGHTED_LAPLACIAN)
+                   {
+                     if (a->ne > 0 && !coeffs)
+                       invalid("weighted Laplacian needs nodal coefficients");
+                     if (coeffs_len < a->ne * (a->dim + 1))
+                       invalid("coefficients shorter than num_elements * (dim+1)");
+                   }
+                   if (a->nnz() > 0 && !values)
+                     invalid("null values buffer");
+                   int dev = 0;
+                   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+                   const DevPlan& p = plan_on(*a, dev);
+                   fbk::AsmArgs ga;
+                   ga.goff = p.goff;
+                   ga.spk = p.spk;
+                   ga.spos = p.spos;
+                   ga.nbr_ptr = p.nbr_ptr;
+                   ga.values = values;
+                   ga.nv = a->nv;
+                   ga.g_in = g;
+                   ga.coeffs = v->op == FB_WEIGHTED_LAPLACIAN ? coeffs : nullptr;
+                   fbk::LaunchSpec s;
+                   s.op = v->op;
+                   s.dim = v->dim;
+                   s.prec = v->cfg.precision;
+                   s.mode = v->cfg.mode;
+                   s.path = v->path;
+                   s.from_g = 1;
+                   cuda_check(fbk::launch_assemble_g(s, ga, v->kp, static_cast<cudaStream_t>(stream)),
+                              "packed assembly kernel launch");
+                 });
+}
+
 int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len, void* values,
                 int64_t nnz, int flags, int device, fb_error* err)
 {

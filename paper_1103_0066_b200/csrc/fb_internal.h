@@ -83,8 +83,13 @@ struct AsmArgs {
   void* values = nullptr;           // CSR values (engine precision)
   int64_t nv = 0;
   int sym = 0;                      // element matrices bitwise symmetric: read columns
+  // G-input assembly (fb_assemble_g.cu): element rows recomputed from the
+  // packed geometry (PackedGeometry layout) instead of read from a store
+  const void* g_in = nullptr;
+  const double* coeffs = nullptr;   // weighted form: ne*(dim+1) nodal coefficients
 };
 cudaError_t launch_assemble(int dim, int nc, int prec, const AsmArgs&, cudaStream_t);
+cudaError_t launch_assemble_g(const LaunchSpec& s, const AsmArgs&, const KParamBlob&, cudaStream_t);
 
 // The same plan built on the GPU from device-resident connectivity
 // (fb_plan.cu); arrays are stream-ordered allocations the caller frees with

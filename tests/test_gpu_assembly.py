@@ -176,3 +176,100 @@ def test_assembly_properties_at_size(op, dim, ne, prec):
         t = (cols % nc == comp).double()  # translation in component `comp`
         r = torch.zeros(plan.rows, dtype=torch.float64, device="cuda").index_add_(0, rows, v64 * t)
         assert r.abs().max().item() <= (1e-4 if prec == "f32" else 1e-12) * scale
+
+
+def fan_mesh(dim, m):
+    """m elements around a hub (2D) or an axis (3D): hub vertices of degree
+    m + dim - 1, above every kernel's shared-memory slot count."""
+    t = 2 * np.pi * np.arange(m) / m
+    if dim == 2:
+        v = np.concatenate([[0.0, 0.0], np.stack([np.cos(t), np.sin(t)], 1).ravel()])
+        c = np.array([[0, 1 + i, 1 + (i + 1) % m] for i in range(m)], dtype=np.int32)
+    else:
+        ring = np.stack([np.cos(t), np.sin(t), 0.3 + 0.1 * np.sin(3 * t)], 1)
+        v = np.concatenate([[0.0, 0.0, 0.0, 0.0, 0.0, 1.0], ring.ravel()])
+        c = np.array([[0, 1, 2 + i, 2 + (i + 1) % m] for i in range(m)], dtype=np.int32)
+    x = v.reshape(-1, dim)[c]
+    j = (x[:, 1:] - x[:, :1]).transpose(0, 2, 1)
+    neg = np.linalg.det(j) < 0
+    c[neg, -2], c[neg, -1] = c[neg, -1].copy(), c[neg, -2].copy()
+    return np.ascontiguousarray(v), np.ascontiguousarray(c.ravel())
+
+
+def _packed_case(var, op, dim, v, c, prec, bs):
+    """(want, got): assemble(integrate_batches(G)) vs assemble_packed(G)."""
+    import torch
+
+    nv, ne = v.size // dim, c.size // (dim + 1)
+    w = coeffs_for(op, v, c, dim)
+    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+    dw = torch.from_numpy(w).cuda() if w is not None else None
+    g = fb.pack_geometry(dv, dc, dim, bs, prec)
+    store = fb.integrate_batches(var, g, ne, dw)
+    plan = fb.AssemblyPlan(op, dim, dc, nv)
+    want = plan.assemble(var, store)
+    got = torch.full_like(want, float("nan"))
+    plan.assemble_packed_async(var, g, got, dw, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return want, got
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("dim,n", [(2, 9), (3, 4)])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_packed_assembly_bitwise(op, dim, n, prec, mode):
+    # assembly straight from packed G == assembly of the integrate_batches store
+    v, c = fb.structured_mesh(dim, n, 0.15, 42)
+    var = fb.make_variant(op, dim, prec, mode, element_batch_size=16)
+    want, got = _packed_case(var, op, dim, v, c, prec, 16)
+    assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_packed_assembly_high_degree_and_general_k(restatement, op, dim, prec):
+    import torch
+
+    # hub vertices beyond the shared-memory slots accumulate in global memory
+    v, c = fan_mesh(dim, 40)
+    var = fb.make_variant(op, dim, prec, "strict", element_batch_size=8)
+    want, got = _packed_case(var, op, dim, v, c, prec, 8)
+    assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+    # a non-symmetric K with the P1 pattern (path 1)
+    k = restatement.build_k(op, dim).copy()
+    nb = dim + 1
+    nc = dim if op == "elasticity" else 1
+    kr = nb * nc
+    k4 = k.reshape(kr, kr, -1, dim * dim)  # [j][i][coefficient][mu*dim + nu]
+    for comp in range(nc):  # (a=1, b=2, mu=0, nu=1) in every component block
+        k4[2 + comp * nb, 1 + comp * nb, 0, 1] *= 1.5
+    var = fb.make_variant(op, dim, prec, "strict", element_batch_size=8, k=k)
+    assert var.path == 1
+    v, c = fb.structured_mesh(dim, 3, 0.15, 7)
+    want, got = _packed_case(var, op, dim, v, c, prec, 8)
+    assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+    del torch
+
+
+def test_packed_assembly_validation(restatement):
+    import torch
+
+    v, c = fb.structured_mesh(3, 2)
+    nv, ne = v.size // 3, c.size // 4
+    plan = fb.AssemblyPlan("laplacian", 3, c, nv)
+    var = fb.make_variant("laplacian", 3, "f64", element_batch_size=1)
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    g = torch.zeros(ne * 9, dtype=torch.float64, device="cuda")
+    with pytest.raises(_lib.InvalidArgument, match="packed geometry shorter"):
+        plan.assemble_packed_async(var, g[:-1], vals)
+    wvar = fb.make_variant("weighted-laplacian", 3, "f64", element_batch_size=1)
+    with pytest.raises(_lib.InvalidArgument, match="nodal coefficients"):
+        plan.assemble_packed_async(wvar, g, vals)
+    dense_k = restatement.build_k("laplacian", 3).copy()
+    dense_k[dense_k == 0] = 0.25  # breaks the P1 pattern: dense path
+    dvar = fb.make_variant("laplacian", 3, "f64", element_batch_size=1, k=dense_k)
+    assert dvar.path == 2
+    with pytest.raises(_lib.InvalidArgument, match="P1 sparsity"):
+        plan.assemble_packed_async(dvar, g, vals)

@@ -86,6 +86,42 @@ def main():
                  "plan_build_host_s": round(t_plan_host, 3)}
             print(json.dumps(r), flush=True)
             res.append(r)
+            # assembly straight from packed G (no element store), and the two
+            # mesh -> CSR pipelines: integrate + assemble vs pack + assemble_packed
+            g = torch.empty(var.store_length(ne) // (kr * kr) * dim * dim, device="cuda", dtype=store.dtype)
+            fb.pack_geometry_async(dv, dc, dim, g, st, var.config.element_batch_size, prec, sid)
+            pv = torch.empty_like(vals)
+
+            def timed(fn):
+                for _ in range(3):
+                    fn()
+                ms = []
+                for _ in range(a.steps):
+                    scrub.view(torch.int64).sum()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                return statistics.median(ms)
+
+            tp = timed(lambda: plan.assemble_packed_async(var, g, pv, None, sid))
+            assert torch.equal(pv, vals), "packed assembly differs from the store assembly"
+            t_store_path = timed(lambda: (fb.integrate_mesh_async(var, dv, dc, store, st, sid),
+                                          plan.assemble_async(var, store, vals, sid, symmetric=True)))
+            t_packed_path = timed(lambda: (fb.pack_geometry_async(dv, dc, dim, g, st, var.config.element_batch_size,
+                                                                  prec, sid),
+                                           plan.assemble_packed_async(var, g, pv, None, sid)))
+            byp = ne * nb * (4 + nb) + 2 * 8 * (nv + 1) + ne * dim * dim * s + plan.nnz * s
+            r = {"workload": w, "kernel": "fb_assemble_g_kernel", "op": op, "dim": dim, "prec": prec,
+                 "ms": round(tp, 4), "algorithmic_bytes": byp, "GBs": round(byp / (tp * 1e-3) * 1e-9),
+                 "frac": round(byp / (tp * 1e-3) * 1e-9 / peak, 3),
+                 "Gelem_s": round(ne / (tp * 1e-3) * 1e-9, 2),
+                 "mesh_to_csr_ms": {"integrate+assemble": round(t_store_path, 4),
+                                    "pack+assemble_packed": round(t_packed_path, 4)}}
+            print(json.dumps(r), flush=True)
+            res.append(r)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "asmbench.json"), "w") as f:
         json.dump(res, f, indent=1)
