@@ -28,6 +28,13 @@ namespace {
 
 constexpr uint32_t kPadG = 0xffffffffu;
 
+#ifndef FB_ASMG_U
+#define FB_ASMG_U 4
+#endif
+#ifndef FB_ASMG_VEC
+#define FB_ASMG_VEC 1
+#endif
+
 template <class S>
 __device__ __forceinline__ S add_rn_g(S a, S b);
 template <>
@@ -42,8 +49,83 @@ struct GShape {
   // neighbours x components accumulated in shared memory (<= 48 KB static)
   static constexpr int FIT = 48 * 1024 / (NC * 32 * WARPS * static_cast<int>(sizeof(S)));
   static constexpr int SLOTS = FIT < 32 ? FIT : 32;
-  static constexpr int U = 4;  // incidences in flight per lane
+  static constexpr int U = FB_ASMG_U;  // incidences in flight per lane
 };
+
+// G_e (DD scalars at gin + e*DD, 4-byte aligned only for 3D f32) with the
+// fewest 16-byte loads: the aligned 16-byte words covering it, then a
+// register select by the misalignment.  The element whose covering words
+// would run past the end of G (ng scalars) is read scalar-wise, and all of
+// G when it is not 16-byte aligned (ng < 0).
+template <class S, int DD>
+__device__ __forceinline__ void load_g(const S* gin, int64_t e, int64_t ng, S (&g)[DD])
+{
+  constexpr int W = 16 / static_cast<int>(sizeof(S));  // scalars per 16-byte word
+  const int64_t first = e * DD;
+  if (!FB_ASMG_VEC || ng < 0)  // ng < 0: G not 16-byte aligned
+  {
+#pragma unroll
+    for (int t = 0; t < DD; ++t)
+      g[t] = __ldg(gin + first + t);
+    return;
+  }
+  if constexpr (DD % W == 0)
+  {
+    // every G_e starts on a 16-byte boundary (G does)
+#pragma unroll
+    for (int t = 0; t < DD; t += W)
+    {
+      if constexpr (W == 4)
+      {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(gin + first + t));
+        g[t] = q.x, g[t + 1] = q.y, g[t + 2] = q.z, g[t + 3] = q.w;
+      }
+      else
+      {
+        const double2 q = __ldg(reinterpret_cast<const double2*>(gin + first + t));
+        g[t] = q.x, g[t + 1] = q.y;
+      }
+    }
+  }
+  else
+  {
+    constexpr int NW = (DD + W - 1 + W - 1) / W;  // words covering any misalignment
+    const int sh = static_cast<int>(first % W);
+    const int64_t w0 = first - sh;
+    if (w0 + NW * W > ng)
+    {
+#pragma unroll
+      for (int t = 0; t < DD; ++t)
+        g[t] = __ldg(gin + first + t);
+      return;
+    }
+    S c[NW * W];
+#pragma unroll
+    for (int k = 0; k < NW; ++k)
+    {
+      if constexpr (W == 4)
+      {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(gin + w0) + k);
+        c[4 * k] = q.x, c[4 * k + 1] = q.y, c[4 * k + 2] = q.z, c[4 * k + 3] = q.w;
+      }
+      else
+      {
+        const double2 q = __ldg(reinterpret_cast<const double2*>(gin + w0) + k);
+        c[2 * k] = q.x, c[2 * k + 1] = q.y;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < DD; ++t)
+    {
+      S x = c[t];
+#pragma unroll
+      for (int r = 1; r < W; ++r)
+        if (t + r < NW * W)
+          x = sh == r ? c[t + r] : x;
+      g[t] = x;
+    }
+  }
+}
 
 // Row aa (runtime) of the nb x nb Laplacian-like block, selected without
 // dynamic register indexing.
@@ -117,9 +199,8 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
       for (int u = 0; u < U; ++u)
       {
         const int64_t e = pk[u] != kPadG ? (pk[u] >> 2) : 0;
-#pragma unroll
-        for (int t = 0; t < DD; ++t)
-          ge[u][t] = pk[u] != kPadG ? __ldg(gin + e * DD + t) : S(0);
+        if (pk[u] != kPadG)
+          load_g<S, DD>(gin, e, a.g_len, ge[u]);
 #pragma unroll
         for (int c = 0; c <= DIM; ++c)
           we[u][c] = OP == kWeighted && pk[u] != kPadG ? static_cast<S>(__ldg(a.coeffs + e * (DIM + 1) + c)) : S(0);

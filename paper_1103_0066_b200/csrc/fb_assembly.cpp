@@ -433,6 +433,8 @@ int fb_assemble_packed_async(const fb_assembly* a, const fb_variant* v, const vo
                      invalid("null packed geometry");
                    if (g_len < a->ne * dd)
                      invalid("packed geometry shorter than num_elements * dim^2");
+                   if (reinterpret_cast<uintptr_t>(g) % scalar_size(v->cfg.precision) != 0)
+                     invalid("packed geometry is not aligned to its scalar size");
                    if (v->op == FB_WEIGHTED_LAPLACIAN)
                    {
                      if (a->ne > 0 && !coeffs)
@@ -452,7 +454,9 @@ int fb_assemble_packed_async(const fb_assembly* a, const fb_variant* v, const vo
                    ga.nbr_ptr = p.nbr_ptr;
                    ga.values = values;
                    ga.nv = a->nv;
+                   // vector loads need a 16-byte aligned G; else the scalar kernel reads it
                    ga.g_in = g;
+                   ga.g_len = (reinterpret_cast<uintptr_t>(g) & 15u) == 0 ? a->ne * dd : -1;
                    ga.coeffs = v->op == FB_WEIGHTED_LAPLACIAN ? coeffs : nullptr;
                    fbk::LaunchSpec s;
                    s.op = v->op;

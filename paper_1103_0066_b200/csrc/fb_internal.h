@@ -87,6 +87,7 @@ struct AsmArgs {
   // packed geometry (PackedGeometry layout) instead of read from a store
   const void* g_in = nullptr;
   const double* coeffs = nullptr;   // weighted form: ne*(dim+1) nodal coefficients
+  int64_t g_len = 0;                // scalars readable at g_in (16-byte aligned)
 };
 cudaError_t launch_assemble(int dim, int nc, int prec, const AsmArgs&, cudaStream_t);
 cudaError_t launch_assemble_g(const LaunchSpec& s, const AsmArgs&, const KParamBlob&, cudaStream_t);

@@ -196,8 +196,9 @@ def fan_mesh(dim, m):
     return np.ascontiguousarray(v), np.ascontiguousarray(c.ravel())
 
 
-def _packed_case(var, op, dim, v, c, prec, bs):
-    """(want, got): assemble(integrate_batches(G)) vs assemble_packed(G)."""
+def _packed_case(var, op, dim, v, c, prec, bs, offset=0):
+    """(want, got): assemble(integrate_batches(G)) vs assemble_packed(G);
+    offset > 0 places G that many scalars into a buffer (misaligned)."""
     import torch
 
     nv, ne = v.size // dim, c.size // (dim + 1)
@@ -205,6 +206,10 @@ def _packed_case(var, op, dim, v, c, prec, bs):
     dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
     dw = torch.from_numpy(w).cuda() if w is not None else None
     g = fb.pack_geometry(dv, dc, dim, bs, prec)
+    if offset:
+        buf = torch.empty(g.numel() + offset, dtype=g.dtype, device="cuda")
+        buf[offset:] = g
+        g = buf[offset:]
     store = fb.integrate_batches(var, g, ne, dw)
     plan = fb.AssemblyPlan(op, dim, dc, nv)
     want = plan.assemble(var, store)
@@ -223,6 +228,12 @@ def test_packed_assembly_bitwise(op, dim, n, prec, mode):
     v, c = fb.structured_mesh(dim, n, 0.15, 42)
     var = fb.make_variant(op, dim, prec, mode, element_batch_size=16)
     want, got = _packed_case(var, op, dim, v, c, prec, 16)
+    assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+    # G not 16-byte aligned (scalar reads) and G of unpadded length (the
+    # last element's covering words would pass the end: read scalar-wise)
+    want, got = _packed_case(var, op, dim, v, c, prec, 16, offset=1)
+    assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+    want, got = _packed_case(var, op, dim, v, c, prec, 1)
     assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
 
 
