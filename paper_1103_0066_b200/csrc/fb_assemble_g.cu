@@ -46,8 +46,8 @@ template <class S, int DIM, int OP>
 struct GShape {
   static constexpr int NC = OP == kElasticity ? DIM : 1;
   static constexpr int WARPS = 4;
-  // neighbours x components accumulated in shared memory (<= 48 KB static)
-  static constexpr int FIT = 48 * 1024 / (NC * 32 * WARPS * static_cast<int>(sizeof(S)));
+  // neighbours accumulated in shared memory (<= 48 KB static)
+  static constexpr int FIT = 48 * 1024 / (32 * WARPS * static_cast<int>(sizeof(S)));
   static constexpr int SLOTS = FIT < 32 ? FIT : 32;
   static constexpr int U = FB_ASMG_U;  // incidences in flight per lane
 };
@@ -144,8 +144,9 @@ __device__ __forceinline__ void select_row(const S (&vv)[NB * NB], int aa, S (&x
 
 // A warp owns 32 consecutive vertices and all their rows.  Elasticity: the
 // element matrix is block diagonal with nc copies of the Laplacian-like
-// block, so each incidence's row is computed once and added to the nc
-// diagonal component blocks; the off-diagonal blocks are written as +0.
+// block, so the nc diagonal component blocks of a CSR row block receive the
+// same additions in the same order: one accumulator per neighbour, written
+// to the nc diagonal entries; the off-diagonal entries are written as +0.
 template <class S, int DIM, int OP, int MODE, bool UNI>
 __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
     fb_assemble_g_kernel(const AsmArgs a, const KP<S, DIM, OP> kp)
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
   using G = GShape<S, DIM, OP>;
   constexpr int NB = DIM + 1, NC = G::NC, DD = DIM * DIM;
   constexpr int T = 32 * G::WARPS, SLOTS = G::SLOTS, U = G::U;
-  __shared__ S acc_s[SLOTS * NC * T];
+  __shared__ S acc_s[SLOTS * T];
   S* acc = acc_s + threadIdx.x;
   S* vals = static_cast<S*>(a.values);
   const S* gin = static_cast<const S*>(a.g_in);
@@ -167,7 +168,6 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
     const int64_t r0 = live ? __ldg(a.nbr_ptr + v) : 0;
     const int deg = live ? static_cast<int>(__ldg(a.nbr_ptr + v + 1) - r0) : 0;
     // CSR row (v, ci) starts at r0*NC*NC + ci*deg*NC; entry (k, cj) at + k*NC + cj.
-    // Diagonal-block accumulator (k, ci) -> acc slot k*NC + ci.
     const int64_t row0 = r0 * NC * NC;
     const bool in_smem = deg <= SLOTS;
     const int64_t q0 = __ldg(a.goff + g), q1 = __ldg(a.goff + g + 1);
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
     };
     load_plan(q0 + lane, pk, ps);
     if (in_smem)
-      for (int k = 0; k < deg * NC; ++k)
+      for (int k = 0; k < deg; ++k)
         acc[k * T] = S(0);
     else
       for (int k = 0; k < deg * NC * NC; ++k)
@@ -217,16 +217,14 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
           for (int b = 0; b < NB; ++b)
           {
             const int k = static_cast<int>((ps[u] >> (8 * b)) & 0xffu);
-#pragma unroll
-            for (int c = 0; c < NC; ++c)
+            if (in_smem)
+              acc[k * T] = add_rn_g(acc[k * T], x[b]);
+            else
             {
-              if (in_smem)
-                acc[(k * NC + c) * T] = add_rn_g(acc[(k * NC + c) * T], x[b]);
-              else
-              {
-                S* p = vals + row0 + static_cast<int64_t>(c) * deg * NC + k * NC + c;
-                *p = add_rn_g(*p, x[b]);
-              }
+              // global accumulation in the (v, 0) row block; copied to the
+              // other diagonal blocks at the end
+              S* p = vals + row0 + k * NC;
+              *p = add_rn_g(*p, x[b]);
             }
           }
         }
@@ -238,11 +236,25 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
       }
     }
     if (in_smem)
-      for (int ci = 0; ci < NC; ++ci)
-        for (int k = 0; k < deg; ++k)
+    {
+      for (int k = 0; k < deg; ++k)
+      {
+        const S x = acc[k * T];
+#pragma unroll
+        for (int ci = 0; ci < NC; ++ci)
 #pragma unroll
           for (int cj = 0; cj < NC; ++cj)
-            vals[row0 + static_cast<int64_t>(ci) * deg * NC + k * NC + cj] = cj == ci ? acc[(k * NC + ci) * T] : S(0);
+            vals[row0 + static_cast<int64_t>(ci) * deg * NC + k * NC + cj] = cj == ci ? x : S(0);
+      }
+    }
+    else if (NC > 1)
+      for (int k = 0; k < deg; ++k)
+      {
+        const S x = vals[row0 + k * NC];
+#pragma unroll
+        for (int ci = 1; ci < NC; ++ci)
+          vals[row0 + static_cast<int64_t>(ci) * deg * NC + k * NC + ci] = x;
+      }
   }
 }
 

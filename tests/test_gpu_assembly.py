@@ -233,7 +233,8 @@ def test_packed_assembly_bitwise(op, dim, n, prec, mode):
     # last element's covering words would pass the end: read scalar-wise)
     want, got = _packed_case(var, op, dim, v, c, prec, 16, offset=1)
     assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
-    want, got = _packed_case(var, op, dim, v, c, prec, 1)
+    var1 = fb.make_variant(op, dim, prec, mode, element_batch_size=1)
+    want, got = _packed_case(var1, op, dim, v, c, prec, 1)
     assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
 
 
