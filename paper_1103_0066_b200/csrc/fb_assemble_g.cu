@@ -142,6 +142,67 @@ __device__ __forceinline__ void select_row(const S (&vv)[NB * NB], int aa, S (&x
       x[b] = aa == r ? vv[r * NB + b] : x[b];
 }
 
+#ifndef FB_ASMG_VECST
+#define FB_ASMG_VECST 1
+#endif
+// Write-out of a vertex's CSR row block (nc rows x deg*nc entries,
+// contiguous, ci-major): entry (ci, k, cj) = acc[k] on the diagonal
+// (cj == ci), +0 elsewhere.  A lane's block is written with 16-byte vector
+// stores between scalar head and tail (a quarter of the L2 write requests of
+// scalar stores: the blocks of a warp's lanes are far apart, so per-lane
+// stores never coalesce).  acc reads are the lane's own shared-memory column
+// ([slot][thread]): conflict-free for any k.
+template <class S, int NC, int T>
+__device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
+{
+  constexpr int W = 16 / static_cast<int>(sizeof(S));
+  const int64_t len = static_cast<int64_t>(deg) * NC * NC;
+  int ci = 0, k = 0, cj = 0;
+  auto next = [&]() -> S
+  {
+    const S x = cj == ci ? acc[k * T] : S(0);
+    if (++cj == NC)
+    {
+      cj = 0;
+      if (++k == deg)
+      {
+        k = 0;
+        ++ci;
+      }
+    }
+    return x;
+  };
+  int64_t p = 0;
+  if (FB_ASMG_VECST)
+  {
+    int64_t head = (W - static_cast<int64_t>((reinterpret_cast<uintptr_t>(base) / sizeof(S)) % W)) % W;
+    head = head < len ? head : len;
+    for (; p < head; ++p)
+      base[p] = next();
+    for (; p + W <= len; p += W)
+    {
+      if constexpr (W == 4)
+      {
+        float4 q;
+        q.x = next();
+        q.y = next();
+        q.z = next();
+        q.w = next();
+        *reinterpret_cast<float4*>(base + p) = q;
+      }
+      else
+      {
+        double2 q;
+        q.x = next();
+        q.y = next();
+        *reinterpret_cast<double2*>(base + p) = q;
+      }
+    }
+  }
+  for (; p < len; ++p)
+    base[p] = next();
+}
+
 // A warp owns 32 consecutive vertices and all their rows.  Elasticity: the
 // element matrix is block diagonal with nc copies of the Laplacian-like
 // block, so the nc diagonal component blocks of a CSR row block receive the
@@ -236,17 +297,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
       }
     }
     if (in_smem)
-    {
-      for (int k = 0; k < deg; ++k)
-      {
-        const S x = acc[k * T];
-#pragma unroll
-        for (int ci = 0; ci < NC; ++ci)
-#pragma unroll
-          for (int cj = 0; cj < NC; ++cj)
-            vals[row0 + static_cast<int64_t>(ci) * deg * NC + k * NC + cj] = cj == ci ? x : S(0);
-      }
-    }
+      write_block<S, NC, T>(vals + row0, deg, acc);
     else if (NC > 1)
       for (int k = 0; k < deg; ++k)
       {
