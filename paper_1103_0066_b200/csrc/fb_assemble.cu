@@ -42,12 +42,15 @@ namespace {
 #ifndef FB_ASM_NCW2
 #define FB_ASM_NCW2 2  // 2D elasticity: a warp reads the whole element row (A/B: 1 is slower)
 #endif
+#ifndef FB_ASM_NCW3D64
+#define FB_ASM_NCW3D64 1  // 3D elasticity FP64
+#endif
 #ifndef FB_ASM_U2D
 #define FB_ASM_U2D FB_ASM_U
 #endif
 template <class S, int DIM, int NC>
 struct AsmShape {
-  static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : 1);
+  static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : (NC == 3 ? FB_ASM_NCW3D64 : 1));
   static constexpr int WARPS = NCW == 1 ? 4 : 2;
   static constexpr int SLOTS = NCW == 1 ? 32 : 24;
   static constexpr int U = DIM == 2 ? FB_ASM_U2D : (NCW == 1 ? FB_ASM_U : 4);
@@ -101,6 +104,33 @@ __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
     else
       r[t] = __ldg(p + t);
   }
+}
+
+#ifndef FB_ASM_VECST
+#define FB_ASM_VECST 1
+#endif
+// base[p] = acc[p*T] for p < len (a lane's own shared-memory column:
+// conflict-free), with 16-byte vector stores between scalar head and tail.
+// The lanes' runs are far apart, so scalar stores would each be a separate
+// L2 write request; vectors cut them by 16 / sizeof(S).
+template <class S, int T>
+__device__ __forceinline__ void write_run(S* base, int len, const S* acc)
+{
+  constexpr int W = 16 / static_cast<int>(sizeof(S));
+  int head = (W - static_cast<int>((reinterpret_cast<uintptr_t>(base) / sizeof(S)) % W)) % W;
+  head = head < len ? head : len;
+  int p = 0;
+  for (; p < head; ++p)
+    base[p] = acc[p * T];
+  for (; p + W <= len; p += W)
+  {
+    if constexpr (W == 4)
+      *reinterpret_cast<float4*>(base + p) = make_float4(acc[p * T], acc[(p + 1) * T], acc[(p + 2) * T], acc[(p + 3) * T]);
+    else
+      *reinterpret_cast<double2*>(base + p) = make_double2(acc[p * T], acc[(p + 1) * T]);
+  }
+  for (; p < len; ++p)
+    base[p] = acc[p * T];
 }
 
 __host__ __device__ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }
@@ -291,9 +321,14 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
       }
     }
     if (in_smem)
-      for (int k = 0; k < deg; ++k)
-        for (int c = 0; c < NCW; ++c)
-          vals[row + k * NC + c] = acc[(k * NCW + c) * T];
+    {
+      if constexpr (NCW == NC && FB_ASM_VECST)
+        write_run<S, T>(vals + row, deg * NC, acc);  // the whole (v, ci) row: contiguous
+      else
+        for (int k = 0; k < deg; ++k)
+          for (int c = 0; c < NCW; ++c)
+            vals[row + k * NC + c] = acc[(k * NCW + c) * T];
+    }
     cur = nxt;
   }
 }
