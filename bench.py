@@ -394,6 +394,42 @@ def main():
             asm = {"ms": max_over_ranks(statistics.mean(a_ms)), "nnz": plan.nnz,
                    "launches": fb.launch_counter() - na0}
 
+            # the same operator straight from packed geometry (no element store),
+            # and the two mesh -> CSR pipelines end to end on the device
+            def dev_timed(fn):
+                for _ in range(max(args.warmup, 1)):
+                    fn()
+                torch.cuda.synchronize()
+                barrier()
+                ms = []
+                clocks.mark()
+                for _ in range(args.steps):
+                    scrub.view(torch.int64).sum()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                clocks.unmark()
+                barrier()
+                return max_over_ranks(statistics.mean(ms))
+
+            g = torch.empty(store_len // (kr * kr) * dim * dim, dtype=tdt, device=dev)
+            gst = torch.empty(2, dtype=torch.int64, device=dev)
+            fb.pack_geometry_async(dv, dc, dim, g, gst, 128, prec, sid)
+            pvals = torch.empty_like(vals)
+            na0 = fb.launch_counter()
+            asm["packed_ms"] = dev_timed(lambda: plan.assemble_packed_async(var, g, pvals, None, sid))
+            asm["packed_launches"] = fb.launch_counter() - na0
+            if args.mode == "strict" and not torch.equal(pvals, vals):  # strict: mesh path == G path
+                raise RuntimeError("packed-geometry assembly differs from the store assembly")
+            asm["pipe_store_ms"] = dev_timed(lambda: (fb.integrate_mesh_async(var, dv, dc, out, gst, sid),
+                                                      plan.assemble_async(var, out, vals, sid,
+                                                                          symmetric=var.path in (0, 3))))
+            asm["pipe_packed_ms"] = dev_timed(lambda: (fb.pack_geometry_async(dv, dc, dim, g, gst, 128, prec, sid),
+                                                       plan.assemble_packed_async(var, g, pvals, None, sid)))
+
     # parity spot check of the timed output (full bitwise check lives in tests/)
     torch.cuda.synchronize()
 
@@ -449,6 +485,16 @@ def main():
             "roofline": {"bound": "hbm", "achieved": a_ach, "peak": peak, "unit": "GB/s", "frac": a_ach / peak,
                          "algorithmic_bytes_per_launch": a_bytes},
             "gpu_launches": asm["launches"]}
+        p_bytes = ne_per * nb_ * (4 + nb_) + 2 * 8 * (nv_all + 1) + ne_per * dim * dim * s_ + asm["nnz"] * s_
+        p_ach = p_bytes / (asm["packed_ms"] * 1e-3) * 1e-9
+        line["assembly"]["from_packed_geometry"] = {
+            "kernel": "fb_assemble_g_kernel (element rows recomputed from packed G, no element store)",
+            "ms_per_step": asm["packed_ms"],
+            "roofline": {"bound": "hbm", "achieved": p_ach, "peak": peak, "unit": "GB/s", "frac": p_ach / peak,
+                         "algorithmic_bytes_per_launch": p_bytes},
+            "gpu_launches": asm["packed_launches"]}
+        line["assembly"]["mesh_to_csr_ms"] = {"integrate_mesh+assemble": asm["pipe_store_ms"],
+                                              "pack_geometry+assemble_packed": asm["pipe_packed_ms"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(op, dim, prec, v, cells)
     if rank == 0:
