@@ -402,6 +402,7 @@ def main():
                 torch.cuda.synchronize()
                 barrier()
                 ms = []
+                n0 = fb.launch_counter()
                 clocks.mark()
                 for _ in range(args.steps):
                     scrub.view(torch.int64).sum()
@@ -413,21 +414,20 @@ def main():
                     ms.append(e0.elapsed_time(e1))
                 clocks.unmark()
                 barrier()
-                return max_over_ranks(statistics.mean(ms))
+                return max_over_ranks(statistics.mean(ms)), fb.launch_counter() - n0
 
             g = torch.empty(store_len // (kr * kr) * dim * dim, dtype=tdt, device=dev)
             gst = torch.empty(2, dtype=torch.int64, device=dev)
             fb.pack_geometry_async(dv, dc, dim, g, gst, 128, prec, sid)
             pvals = torch.empty_like(vals)
-            na0 = fb.launch_counter()
-            asm["packed_ms"] = dev_timed(lambda: plan.assemble_packed_async(var, g, pvals, None, sid))
-            asm["packed_launches"] = fb.launch_counter() - na0
+            asm["packed_ms"], asm["packed_launches"] = dev_timed(
+                lambda: plan.assemble_packed_async(var, g, pvals, None, sid))
             if args.mode == "strict" and not torch.equal(pvals, vals):  # strict: mesh path == G path
                 raise RuntimeError("packed-geometry assembly differs from the store assembly")
-            asm["pipe_store_ms"] = dev_timed(lambda: (fb.integrate_mesh_async(var, dv, dc, out, gst, sid),
+            asm["pipe_store_ms"], _ = dev_timed(lambda: (fb.integrate_mesh_async(var, dv, dc, out, gst, sid),
                                                       plan.assemble_async(var, out, vals, sid,
                                                                           symmetric=var.path in (0, 3))))
-            asm["pipe_packed_ms"] = dev_timed(lambda: (fb.pack_geometry_async(dv, dc, dim, g, gst, 128, prec, sid),
+            asm["pipe_packed_ms"], _ = dev_timed(lambda: (fb.pack_geometry_async(dv, dc, dim, g, gst, 128, prec, sid),
                                                        plan.assemble_packed_async(var, g, pvals, None, sid)))
 
     # parity spot check of the timed output (full bitwise check lives in tests/)
