@@ -273,6 +273,11 @@ int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* sto
 int fb_assemble_packed_async(const fb_assembly* a, const fb_variant* v, const void* g, int64_t g_len,
                              const double* coeffs, int64_t coeffs_len, void* values, int64_t nnz,
                              void* stream, fb_error* err);
+/* Synchronous form: g, coeffs, values host or device pointers (host data is
+ * staged through the device of `device`, or of the device-resident input). */
+int fb_assemble_packed(const fb_assembly* a, const fb_variant* v, const void* g, int64_t g_len,
+                       const double* coeffs, int64_t coeffs_len, void* values, int64_t nnz, int device,
+                       fb_error* err);
 
 #ifdef __cplusplus
 }

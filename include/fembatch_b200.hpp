@@ -252,5 +252,10 @@ AssemblyPlan make_assembly_plan(Operator op, const Mesh& mesh);
 // (true for integrate_mesh output of the reference forms), read as columns.
 CsrMatrix assemble_global(const KernelVariant& variant, const AssemblyPlan& plan, const ElementMatrixStore& store,
                           bool symmetric = false, int device = 0);
+// The same operator straight from packed geometry (fb_assemble_packed): the
+// element matrices are recomputed per incidence and never stored; bitwise
+// assemble_global(integrate_batches(geometry)).  Needs a P1-pattern K.
+CsrMatrix assemble_global(const KernelVariant& variant, const AssemblyPlan& plan, const PackedGeometry& geometry,
+                          const std::vector<double>& coefficients = {}, int device = 0);
 
 }  // namespace fembatch

@@ -92,6 +92,26 @@ class AssemblyPlan:
                                          C.c_void_p(stream), C.byref(err))
         L.raise_for(rc, err)
 
+    def assemble_packed(self, variant: KernelVariant, g, coeffs=None, values=None, device: int = 0):
+        """CSR values straight from packed geometry ``g`` (host or device; the
+        ``integrate_batches`` input): bitwise ``assemble(integrate_batches(g))``
+        without ever storing the element matrices."""
+        g = _as(g, variant.dtype)
+        coeffs = _as(coeffs, np.float64)
+        if values is None:
+            if _is_torch(g) and g.is_cuda:
+                import torch
+                values = torch.empty(self.nnz, device=g.device,
+                                     dtype=torch.float32 if variant.dtype == np.float32 else torch.float64)
+            else:
+                values = np.empty(self.nnz, dtype=variant.dtype)
+        err = L.fb_error()
+        rc = self._lib.fb_assemble_packed(self._h, variant.handle, _ptr(g), _numel(g), _ptr(coeffs),
+                                          _numel(coeffs) if coeffs is not None else 0, _ptr(values),
+                                          _numel(values), device, C.byref(err))
+        L.raise_for(rc, err)
+        return values
+
     def assemble_packed_async(self, variant: KernelVariant, g, values, coeffs=None, stream: int = 0):
         """Enqueue assembly straight from packed geometry ``g`` (the
         ``integrate_batches`` input, device tensor in engine precision): the

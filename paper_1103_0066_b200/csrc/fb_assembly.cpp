@@ -338,6 +338,55 @@ void launch_on(const fb_assembly& A, const fb_variant& v, const void* store, voi
   cuda_check(fbk::launch_assemble(A.dim, A.nc, v.cfg.precision, g, st), "assemble kernel launch");
 }
 
+void check_packed(const fb_assembly* a, const fb_variant* v, const void* g, int64_t g_len, const double* coeffs,
+                  int64_t coeffs_len, const void* values, int64_t nnz)
+{
+  check_pair(a, v, a ? a->ne * (v ? v->krows * v->krows : 0) : 0, nnz);
+  const int64_t dd = static_cast<int64_t>(a->dim) * a->dim;
+  if (v->path == fbk::kDense)
+    invalid("packed-geometry assembly needs a K with the P1 sparsity pattern");
+  if (a->ne > 0 && !g)
+    invalid("null packed geometry");
+  if (g_len < a->ne * dd)
+    invalid("packed geometry shorter than num_elements * dim^2");
+  if (reinterpret_cast<uintptr_t>(g) % scalar_size(v->cfg.precision) != 0)
+    invalid("packed geometry is not aligned to its scalar size");
+  if (v->op == FB_WEIGHTED_LAPLACIAN)
+  {
+    if (a->ne > 0 && !coeffs)
+      invalid("weighted Laplacian needs nodal coefficients");
+    if (coeffs_len < a->ne * (a->dim + 1))
+      invalid("coefficients shorter than num_elements * (dim+1)");
+  }
+  if (a->nnz() > 0 && !values)
+    invalid("null values buffer");
+}
+
+void launch_packed_on(const fb_assembly& A, const fb_variant& v, const void* g, const double* coeffs, void* values,
+                      int dev, cudaStream_t st)
+{
+  const DevPlan& p = plan_on(A, dev);
+  fbk::AsmArgs ga;
+  ga.goff = p.goff;
+  ga.spk = p.spk;
+  ga.spos = p.spos;
+  ga.nbr_ptr = p.nbr_ptr;
+  ga.values = values;
+  ga.nv = A.nv;
+  // vector loads need a 16-byte aligned G; else the kernel reads it scalar-wise
+  ga.g_in = g;
+  ga.g_len = (reinterpret_cast<uintptr_t>(g) & 15u) == 0 ? A.ne * A.dim * A.dim : -1;
+  ga.coeffs = v.op == FB_WEIGHTED_LAPLACIAN ? coeffs : nullptr;
+  fbk::LaunchSpec s;
+  s.op = v.op;
+  s.dim = v.dim;
+  s.prec = v.cfg.precision;
+  s.mode = v.cfg.mode;
+  s.path = v.path;
+  s.from_g = 1;
+  cuda_check(fbk::launch_assemble_g(s, ga, v.kp, st), "packed assembly kernel launch");
+}
+
 }  // namespace
 
 extern "C" {
@@ -425,48 +474,78 @@ int fb_assemble_packed_async(const fb_assembly* a, const fb_variant* v, const vo
   return guarded(err,
                  [&]
                  {
-                   check_pair(a, v, a ? a->ne * (v ? v->krows * v->krows : 0) : 0, nnz);
-                   const int64_t dd = static_cast<int64_t>(a->dim) * a->dim;
-                   if (v->path == fbk::kDense)
-                     invalid("packed-geometry assembly needs a K with the P1 sparsity pattern");
-                   if (a->ne > 0 && !g)
-                     invalid("null packed geometry");
-                   if (g_len < a->ne * dd)
-                     invalid("packed geometry shorter than num_elements * dim^2");
-                   if (reinterpret_cast<uintptr_t>(g) % scalar_size(v->cfg.precision) != 0)
-                     invalid("packed geometry is not aligned to its scalar size");
-                   if (v->op == FB_WEIGHTED_LAPLACIAN)
-                   {
-                     if (a->ne > 0 && !coeffs)
-                       invalid("weighted Laplacian needs nodal coefficients");
-                     if (coeffs_len < a->ne * (a->dim + 1))
-                       invalid("coefficients shorter than num_elements * (dim+1)");
-                   }
-                   if (a->nnz() > 0 && !values)
-                     invalid("null values buffer");
+                   check_packed(a, v, g, g_len, coeffs, coeffs_len, values, nnz);
                    int dev = 0;
                    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-                   const DevPlan& p = plan_on(*a, dev);
-                   fbk::AsmArgs ga;
-                   ga.goff = p.goff;
-                   ga.spk = p.spk;
-                   ga.spos = p.spos;
-                   ga.nbr_ptr = p.nbr_ptr;
-                   ga.values = values;
-                   ga.nv = a->nv;
-                   // vector loads need a 16-byte aligned G; else the scalar kernel reads it
-                   ga.g_in = g;
-                   ga.g_len = (reinterpret_cast<uintptr_t>(g) & 15u) == 0 ? a->ne * dd : -1;
-                   ga.coeffs = v->op == FB_WEIGHTED_LAPLACIAN ? coeffs : nullptr;
-                   fbk::LaunchSpec s;
-                   s.op = v->op;
-                   s.dim = v->dim;
-                   s.prec = v->cfg.precision;
-                   s.mode = v->cfg.mode;
-                   s.path = v->path;
-                   s.from_g = 1;
-                   cuda_check(fbk::launch_assemble_g(s, ga, v->kp, static_cast<cudaStream_t>(stream)),
-                              "packed assembly kernel launch");
+                   launch_packed_on(*a, *v, g, coeffs, values, dev, static_cast<cudaStream_t>(stream));
+                 });
+}
+
+int fb_assemble_packed(const fb_assembly* a, const fb_variant* v, const void* g, int64_t g_len,
+                       const double* coeffs, int64_t coeffs_len, void* values, int64_t nnz, int device,
+                       fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   check_packed(a, v, g, g_len, coeffs, coeffs_len, values, nnz);
+                   if (device_count() == 0)
+                     throw_code(FB_ERR_NO_DEVICE, "no CUDA device available");
+                   const int gdev = pointer_device(g), vdev = pointer_device(values);
+                   const int dev = gdev >= 0 ? gdev : (vdev >= 0 ? vdev : std::max(device, 0));
+                   const bool weighted = v->op == FB_WEIGHTED_LAPLACIAN;
+                   const int cdev = weighted ? pointer_device(coeffs) : dev;
+                   int cur = 0;
+                   cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+                   cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+                   const size_t ss = scalar_size(v->cfg.precision);
+                   const size_t gbytes = static_cast<size_t>(a->ne) * a->dim * a->dim * ss;
+                   const size_t cbytes = static_cast<size_t>(a->ne) * (a->dim + 1) * sizeof(double);
+                   const size_t vbytes = static_cast<size_t>(nnz) * ss;
+                   std::vector<void*> tmp;
+                   cudaStream_t st = nullptr;
+                   auto stage_in = [&](const void* src, size_t bytes) -> void*
+                   {
+                     void* d = nullptr;
+                     cuda_check(cudaMalloc(&d, std::max<size_t>(bytes, 16)), "cudaMalloc");
+                     tmp.push_back(d);
+                     if (bytes)
+                       cuda_check(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, st), "upload");
+                     return d;
+                   };
+                   auto cleanup = [&]
+                   {
+                     if (st)
+                       cudaStreamSynchronize(st);
+                     for (void* p : tmp)
+                       cudaFree(p);
+                     if (st)
+                       cudaStreamDestroy(st);
+                     cudaSetDevice(cur);
+                   };
+                   try
+                   {
+                     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+                     const void* dg = gdev == dev ? g : stage_in(g, gbytes);
+                     const double* dc =
+                         !weighted || cdev == dev ? coeffs : static_cast<const double*>(stage_in(coeffs, cbytes));
+                     void* dv = values;
+                     if (vdev != dev)
+                     {
+                       cuda_check(cudaMalloc(&dv, std::max<size_t>(vbytes, 16)), "cudaMalloc");
+                       tmp.push_back(dv);
+                     }
+                     launch_packed_on(*a, *v, dg, dc, dv, dev, st);
+                     if (vdev != dev && vbytes)
+                       cuda_check(cudaMemcpyAsync(values, dv, vbytes, cudaMemcpyDefault, st), "download values");
+                     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+                   }
+                   catch (...)
+                   {
+                     cleanup();
+                     throw;
+                   }
+                   cleanup();
                  });
 }
 

@@ -703,4 +703,28 @@ CsrMatrix assemble_global(const KernelVariant& v, const AssemblyPlan& plan, cons
   return m;
 }
 
+CsrMatrix assemble_global(const KernelVariant& v, const AssemblyPlan& plan, const PackedGeometry& geometry,
+                          const std::vector<double>& coefficients, int device)
+{
+  if (!v.device || !plan.device)
+    throw std::invalid_argument("variant or assembly plan was not created for the GPU");
+  if (geometry.precision != v.config.precision || geometry.dim != plan.dim)
+    throw std::invalid_argument("packed geometry does not match variant / plan");
+  CsrMatrix m;
+  m.rows = plan.rows;
+  m.precision = geometry.precision;
+  m.row_ptr.resize(plan.rows + 1);
+  m.col_idx.resize(plan.nnz);
+  fb_error err{};
+  check(fb_assembly_pattern(plan.device.get(), m.row_ptr.data(), plan.rows + 1, m.col_idx.data(), plan.nnz, &err),
+        err);
+  m.values = make_scalar_array(geometry.precision, plan.nnz);
+  check(fb_assemble_packed(plan.device.get(), v.device.get(), data_ptr(geometry.data),
+                           scalar_array_size(geometry.data), coefficients.empty() ? nullptr : coefficients.data(),
+                           static_cast<std::int64_t>(coefficients.size()), data_ptr(m.values), plan.nnz, device,
+                           &err),
+        err);
+  return m;
+}
+
 }  // namespace fembatch

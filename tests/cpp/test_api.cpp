@@ -487,6 +487,15 @@ TEST_CASE(global_assembly_is_the_serial_element_sum, true)
         same = scalar_array_at(a.values, z) == w && scalar_array_at(b.values, z) == w;
       }
       CHECK(same);
+      // the same operator straight from packed geometry (no element store)
+      const PackedGeometry geom = pack_geometry(mesh, c);
+      const CsrMatrix g = assemble_global(v, plan, geom);
+      const CsrMatrix gs = assemble_global(v, plan, integrate_batches(v, geom));
+      bool gsame = g.values.index() == gs.values.index();
+      for (std::int64_t z = 0; gsame && z < plan.nnz; ++z)
+        gsame = scalar_array_at(g.values, z) == scalar_array_at(gs.values, z) &&
+                scalar_array_at(g.values, z) == scalar_array_at(a.values, z);
+      CHECK(gsame);
     }
 }
 

@@ -216,6 +216,10 @@ def _packed_case(var, op, dim, v, c, prec, bs, offset=0):
     got = torch.full_like(want, float("nan"))
     plan.assemble_packed_async(var, g, got, dw, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
+    # synchronous API: host buffers (staged) and device tensors
+    host = plan.assemble_packed(var, g.cpu().numpy(), w)
+    assert host.tobytes() == want.cpu().numpy().tobytes()
+    assert torch.equal(plan.assemble_packed(var, g, dw), want)
     return want, got
 
 
