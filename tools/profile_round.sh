@@ -8,6 +8,9 @@ tag=${1:-r01}
 o=gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $o/${tag}_smi.txt
 timeout 600 python bench.py > $o/${tag}_bench_default.json 2> $o/${tag}_bench_default.err
+for w in 3d-laplacian-16m 3d-elasticity-8m 2d-laplacian-64k; do
+  timeout 600 python bench.py --workload $w --no-cpu-baseline > $o/${tag}_bench_$w.json 2> $o/${tag}_bench_$w.err
+done
 timeout 600 python bench.py --impl reference > $o/${tag}_bench_impl_reference.json 2> $o/${tag}_bench_ref.err
 timeout 300 python tools/hbm_probe.py $o/${tag}_hbm_probe.json > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/${tag}_launches_bench_default.csv \
@@ -18,8 +21,10 @@ for w in 2d-elasticity-1m 3d-laplacian-16m 3d-elasticity-8m; do
         -o $o/${tag}_ncu_${w}_${p} python tools/run_kernel.py --workload $w --precision $p --reps 2 > /dev/null 2>&1
   done
 done
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_assemble -s 1 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_assemble_kernel -s 1 -c 1 \
     -o $o/${tag}_ncu_assemble_3d-laplacian-16m_f32 python tools/asmbench.py --workloads 3d-laplacian-16m --precisions f32 --steps 1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_assemble_g_kernel -s 1 -c 1 \
+    -o $o/${tag}_ncu_assemble_packed_3d-elasticity-8m_f32 python tools/asmbench.py --workloads 3d-elasticity-8m --precisions f32 --steps 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:fb_integrate_sparse<float, .int.3, .int.3," -s 1 -c 1 \
     -o $o/${tag}_ncu_pack_geometry_3d_f32 python tools/pathbench.py --precisions f32 --steps 1 > /dev/null 2>&1
 timeout 500 python tools/asmbench.py > $o/${tag}_asmbench.txt 2>&1
