@@ -35,6 +35,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# ~100 us device-side spin before each timed launch (outside the events)
+GAP_CYCLES = 200_000
+
 WORKLOADS = {
     # name: (op, dim, elements per GPU, BASELINE.json config string)
     "2d-elasticity-1m": ("elasticity", 2, 1 << 20,
@@ -322,6 +325,10 @@ def main():
         clocks.mark()
         for i in range(k):
             scrub.view(torch.int64).sum()  # flush L2 with clean lines (outside the events)
+            # keep the device queue ahead of the host: the start event is then
+            # stamped when the launch is already enqueued, so no host launch
+            # latency lands inside the device-timed window (outside the events)
+            torch.cuda._sleep(GAP_CYCLES)
             starts[i].record(stream)
             fb.integrate_mesh_async(variant, dv, dc, output, status, sid)
             ends[i].record(stream)
@@ -383,6 +390,7 @@ def main():
             clocks.mark()
             for _ in range(args.steps):
                 scrub.view(torch.int64).sum()
+                torch.cuda._sleep(GAP_CYCLES)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 plan.assemble_async(var, out, vals, sid, symmetric=var.path in (0, 3))
@@ -406,6 +414,7 @@ def main():
                 clocks.mark()
                 for _ in range(args.steps):
                     scrub.view(torch.int64).sum()
+                    torch.cuda._sleep(GAP_CYCLES)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn()

@@ -69,6 +69,7 @@ def main():
             ms = []
             for _ in range(a.steps):
                 scrub.view(torch.int64).sum()
+                torch.cuda._sleep(bench.GAP_CYCLES)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 plan.assemble_async(var, store, vals, sid, symmetric=True)
@@ -98,6 +99,7 @@ def main():
                 ms = []
                 for _ in range(a.steps):
                     scrub.view(torch.int64).sum()
+                    torch.cuda._sleep(bench.GAP_CYCLES)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn()

@@ -54,6 +54,7 @@ def main():
                     ms = []
                     for _ in range(a.steps):
                         scrub.view(torch.int64).sum()
+                        torch.cuda._sleep(bench.GAP_CYCLES)
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record()
                         fb.integrate_mesh_async(var, dv, dc, out, st, sid)
