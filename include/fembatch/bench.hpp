@@ -1,0 +1,4 @@
+// Drop-in forwarding header: code written against the reference's
+// "fembatch/bench.hpp" compiles unchanged against the B200 engine.
+#pragma once
+#include "../fembatch_b200.hpp"
