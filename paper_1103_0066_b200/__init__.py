@@ -30,6 +30,7 @@ from .engine import (  # noqa: F401
 )
 from .assembly import AssemblyPlan, assemble, assembly_plan  # noqa: F401
 from .mesh import jitter_mesh, mesh_prefix, structured_mesh  # noqa: F401
-from .storeio import read_mesh_text, read_store, write_mesh_text, write_store  # noqa: F401
+from .storeio import (read_bench_csv, read_mesh_text, read_store, write_bench_csv, write_bench_json,  # noqa: F401
+                      write_mesh_text, write_store)
 
 __version__ = "0.1.0"

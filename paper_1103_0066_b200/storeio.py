@@ -87,3 +87,103 @@ def read_mesh_text(path: str):
 
 def _g17(x: float) -> str:
     return "%.17g" % x
+
+
+# ---------------------------------------------------------------- bench records
+# The reference's benchmark table (src/bench.cpp:231-384; the C++ layer's
+# write_csv / read_csv / write_json): 15 fields, string fields quoted with
+# doubled quotes, flags "on"/"off", doubles at 17 significant digits.
+CSV_HEADER = ("operator,dim,num_elements,batch_size,concurrent,interleave,unroll,"
+              "precision,workers,reps,seconds_min,seconds_mean,gflops,checksum,status")
+_FIELDS = CSV_HEADER.split(",")
+_INT = {"dim", "num_elements", "batch_size", "concurrent", "workers", "reps"}
+_FLT = {"seconds_min", "seconds_mean", "gflops", "checksum"}
+_FLAG = {"interleave", "unroll"}
+
+
+def _q(s: str) -> str:
+    return '"' + s.replace('"', '""') + '"'
+
+
+def write_bench_csv(path: str, records) -> None:
+    """records: dicts keyed by the CSV field names (flags as bools)."""
+    with open(path, "w", newline="") as f:
+        f.write(CSV_HEADER + "\n")
+        for r in records:
+            out = []
+            for k in _FIELDS:
+                v = r[k]
+                if k in _FLAG:
+                    out.append(_q("on" if v else "off"))
+                elif k in _FLT:
+                    out.append(_g17(float(v)))
+                elif k in _INT:
+                    out.append(str(int(v)))
+                else:
+                    out.append(_q(str(v)))
+            f.write(",".join(out) + "\n")
+
+
+def _split(line: str):
+    fields, cur, q, i = [], "", False, 0
+    while i < len(line):
+        ch = line[i]
+        if q:
+            if ch == '"':
+                if i + 1 < len(line) and line[i + 1] == '"':
+                    cur += '"'
+                    i += 1
+                else:
+                    q = False
+            else:
+                cur += ch
+        elif ch == '"':
+            q = True
+        elif ch == ",":
+            fields.append(cur)
+            cur = ""
+        else:
+            cur += ch
+        i += 1
+    fields.append(cur)
+    return fields
+
+
+def read_bench_csv(path: str):
+    """Records as dicts; the reference reader's errors (ValueError here)."""
+    with open(path, newline="") as f:
+        lines = f.read().split("\n")
+    if not lines or lines == [""]:
+        raise ValueError("empty benchmark table")
+    if lines[0].rstrip("\r") != CSV_HEADER:
+        raise ValueError("unrecognized benchmark table header")
+    out = []
+    for line in lines[1:]:
+        line = line.rstrip("\r")
+        if not line:
+            continue
+        f = _split(line)
+        if len(f) != 15:
+            raise ValueError(f"benchmark table row has {len(f)} fields, expected 15")
+        r = {}
+        for k, v in zip(_FIELDS, f):
+            if k in _FLAG:
+                if v not in ("on", "off"):
+                    raise ValueError(f"bad flag field '{v}' (want on/off)")
+                r[k] = v == "on"
+            elif k in _INT:
+                r[k] = int(v)
+            elif k in _FLT:
+                r[k] = float(v)
+            else:
+                r[k] = v
+        out.append(r)
+    return out
+
+
+def write_bench_json(path: str, records) -> None:
+    """Array of objects in CSV field order, flags as "on"/"off"."""
+    import json
+    rows = [{k: (("on" if r[k] else "off") if k in _FLAG else r[k]) for k in _FIELDS} for r in records]
+    with open(path, "w") as f:
+        f.write(json.dumps(rows, indent=2) + "\n")

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <fstream>
 #include <iterator>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <sstream>
@@ -445,6 +446,36 @@ TEST_CASE(assembly_plan_pattern_and_validation, false)
   bad.cells[5] = bad.cells[3];  // cell 1 repeats a vertex
   CHECK_THROWS_WITH_AS(make_assembly_plan(Operator::laplacian, bad), "repeated vertex in cell 1",
                        std::invalid_argument);
+}
+
+// F4 bench records against the reference CLI's own sweep table
+// (tests/golden/ref_bench_sweep.csv): read back and re-written byte for byte;
+// the JSON form of the same records goes to $FB_TEST_JSON_OUT when set
+// (tests/test_cpp_api.py compares it with the Python writer, which is pinned
+// to the reference's JSON bytes), and the reader rejects malformed tables.
+TEST_CASE(bench_records_round_trip, false)
+{
+  const std::string csv = slurp(g_golden + "/ref_bench_sweep.csv");
+  CHECK(!csv.empty());
+  std::istringstream in(csv);
+  const std::vector<BenchRecord> recs = read_csv(in);
+  CHECK(recs.size() == 16 && recs[0].op == "laplacian" && recs[4].status == "invalid: divisibility");
+  std::ostringstream out;
+  write_csv(out, recs);
+  CHECK(out.str() == csv);
+  if (const char* path = std::getenv("FB_TEST_JSON_OUT"))
+  {
+    std::ofstream f(path, std::ios::binary);
+    write_json(f, recs);
+  }
+  for (const char* bad : {"", "wrong,header\n", "operator,dim,num_elements,batch_size,concurrent,interleave,unroll,"
+                                                 "precision,workers,reps,seconds_min,seconds_mean,gflops,checksum,"
+                                                 "status\n\"laplacian\",2\n"})
+  {
+    std::istringstream b(bad);
+    CHECK_THROWS_AS(read_csv(b), std::runtime_error);
+  }
+  CHECK(default_tolerance(Precision::f64) == 1e-12 && default_tolerance(Precision::f32) == 5e-5);
 }
 
 TEST_CASE(global_assembly_is_the_serial_element_sum, true)

@@ -97,7 +97,25 @@ def main():
     for name, (op, dim, n, jit, bs, ce, prec) in FILES.items():
         ref.write_files(op, dim, n, jit, 42, bs, ce, prec, os.path.join(here, f"{name}.fbemat"),
                         os.path.join(here, f"{name}.mesh"))
+    bench_records(here)
+
+
+def bench_records(here):
+    """F4 bench records: the reference CLI's sweep table as CSV and as JSON
+    (two runs: timings differ, formats are what the tests pin)."""
+    import subprocess
+
+    cli = os.path.join(ROOT, "oracle", "_ref", "fembatch_cli_reference")
+    if not os.path.exists(cli):
+        return
+    for fmt in ("csv", "json"):
+        subprocess.run([cli, "sweep", "--operator", "laplacian", "--dim", "2", "--n", "4", "--batch-size", "16,32",
+                        "--concurrent", "1,3", "--reps", "2", "--format", fmt, "--output",
+                        os.path.join(here, f"ref_bench_sweep.{fmt}")], check=True, timeout=600)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--bench-records"]:
+        bench_records(os.path.dirname(os.path.abspath(__file__)))
+    else:
+        main()

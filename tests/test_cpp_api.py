@@ -17,10 +17,19 @@ def _binary(path=BIN):
     return path
 
 
-def test_cpp_api_host_cases():
-    r = subprocess.run([_binary(), "cpu", GOLDEN], capture_output=True, text=True, timeout=300)
+def test_cpp_api_host_cases(tmp_path):
+    js = tmp_path / "bench.json"
+    r = subprocess.run([_binary(), "cpu", GOLDEN], capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "FB_TEST_JSON_OUT": str(js)})
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+    # the C++ write_json equals the Python writer (pinned to the reference's
+    # JSON bytes in tests/test_storeio.py) on the same records
+    import paper_1103_0066_b200 as fb
+
+    py = tmp_path / "py.json"
+    fb.write_bench_json(str(py), fb.read_bench_csv(os.path.join(GOLDEN, "ref_bench_sweep.csv")))
+    assert js.read_bytes() == py.read_bytes()
 
 
 @pytest.mark.gpu

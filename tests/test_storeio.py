@@ -54,3 +54,36 @@ def test_gpu_store_written_equals_reference_file(tmp_path, name):
     out = tmp_path / "s.fbemat"
     storeio.write_store(str(out), store, dim, var.spec.krows, bs, c.size // (dim + 1), ce)
     assert out.read_bytes() == open(os.path.join(GOLDEN, name + ".fbemat"), "rb").read()
+
+
+# F4 bench records: the reference CLI's sweep table (tests/golden/make_golden.py
+# --bench-records) read and re-written byte for byte, CSV and JSON.
+def test_bench_csv_round_trip_is_byte_exact(tmp_path):
+    src = os.path.join(GOLDEN, "ref_bench_sweep.csv")
+    recs = fb.read_bench_csv(src)
+    assert len(recs) == 16 and recs[0]["operator"] == "laplacian" and recs[0]["interleave"] is False
+    assert recs[4]["status"] == "invalid: divisibility" and recs[4]["gflops"] == 0.0
+    out = tmp_path / "b.csv"
+    fb.write_bench_csv(str(out), recs)
+    assert out.read_bytes() == open(src, "rb").read()
+
+
+def test_bench_json_matches_reference_bytes(tmp_path):
+    import json
+
+    src = os.path.join(GOLDEN, "ref_bench_sweep.json")
+    rows = json.load(open(src))
+    recs = [{**r, "interleave": r["interleave"] == "on", "unroll": r["unroll"] == "on"} for r in rows]
+    out = tmp_path / "b.json"
+    fb.write_bench_json(str(out), recs)
+    assert out.read_bytes() == open(src, "rb").read()
+
+
+def test_bench_csv_reader_rejects_malformed(tmp_path):
+    cases = ["", "wrong,header\n", fb.storeio.CSV_HEADER + '\n"laplacian",2\n',
+             fb.storeio.CSV_HEADER + '\n"laplacian",2,32,16,1,"maybe","off","f32",1,1,0,0,0,0,"ok"\n']
+    for i, text in enumerate(cases):
+        p = tmp_path / f"bad{i}.csv"
+        p.write_text(text)
+        with pytest.raises(ValueError):
+            fb.read_bench_csv(str(p))
