@@ -5,7 +5,9 @@ racecheck / synccheck):
 
 Covers the fused integration (every op x dim x precision x store path,
 ragged tile counts, unaligned output), GPU pack_geometry, the G-input path,
-the GPU assembly plan build and the assembly kernel.
+the GPU assembly plan build and both assembly kernels (store and packed G,
+incl. hub vertices beyond the shared-memory slots).  Run with
+PYTORCH_NO_CUDA_MEMORY_CACHING=1 so every buffer is its own allocation.
 """
 import os
 import sys
@@ -48,6 +50,33 @@ def main():
                 for sym in (False, True):
                     vals = torch.empty(plan.nnz, dtype=dt, device="cuda")
                     plan.assemble_async(var, out, vals, sid, symmetric=sym)
+                # assembly from packed G: G of exactly ne*dim^2 scalars (the
+                # vector loads' tail guard), aligned and misaligned
+                gx = torch.empty(ne * dim * dim + 1, dtype=dt, device="cuda")
+                for gg in (gx[:-1], gx[1:]):
+                    gg.copy_(g[: ne * dim * dim])
+                    plan.assemble_packed_async(var, gg, vals, coeffs, sid)
+                torch.cuda.synchronize()
+    # hub vertices beyond the shared-memory slots (global accumulation paths)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_gpu_assembly import fan_mesh
+
+    for dim in (2, 3):
+        v, c = fan_mesh(dim, 40)
+        ne = c.size // (dim + 1)
+        dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+        for prec in ("f32", "f64"):
+            dt = torch.float32 if prec == "f32" else torch.float64
+            for op in ("laplacian", "elasticity"):
+                var = fb.make_variant(op, dim, prec, "strict", element_batch_size=8)
+                g = torch.empty(var.store_length(ne) // var.spec.krows ** 2 * dim * dim, dtype=dt, device="cuda")
+                fb.pack_geometry_async(dv, dc, dim, g, st, 8, prec, sid)
+                out = torch.empty(var.store_length(ne), dtype=dt, device="cuda")
+                fb.integrate_packed_async(var, g, ne, out, sid)
+                plan = fb.AssemblyPlan(op, dim, dc, v.size // dim)
+                vals = torch.empty(plan.nnz, dtype=dt, device="cuda")
+                plan.assemble_async(var, out, vals, sid, symmetric=True)
+                plan.assemble_packed_async(var, g, vals, None, sid)
                 torch.cuda.synchronize()
     print("sanitize run ok")
 
