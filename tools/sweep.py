@@ -14,6 +14,7 @@ changes values, not bytes or flops).  Points whose per-GPU store exceeds
 import argparse
 import csv
 import os
+import shutil
 import statistics
 import sys
 
@@ -117,6 +118,9 @@ def main():
                     f.flush()
                     print(row, flush=True)
     f.close()
+    # a copy the GPU-box runner brings back
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    shutil.copy(path, os.path.join(ROOT, "gpurun_out", a.out + ".csv"))
     print("wrote", path)
 
 
