@@ -340,7 +340,10 @@ cudaError_t go(const AsmArgs& a, cudaStream_t st)
   const int64_t nwarps = (a.nv + 31) / 32 * NC * (NC / AsmShape<S, DIM, NC>::NCW);
   if (nwarps <= 0)
     return cudaSuccess;
-  static int grid_cap = 0;
+  // resident CTAs per SM x SMs, computed once per instantiation (reentrant:
+  // concurrent first calls compute the same value)
+  static std::atomic<int> grid_cap_cache{0};
+  int grid_cap = grid_cap_cache.load(std::memory_order_relaxed);
   if (grid_cap == 0)
   {
     int blocks = 0, dev = 0, sms = 0;
@@ -348,6 +351,7 @@ cudaError_t go(const AsmArgs& a, cudaStream_t st)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid_cap = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
+    grid_cap_cache.store(grid_cap, std::memory_order_relaxed);
   }
   const int64_t need = (nwarps + T / 32 - 1) / (T / 32);
   const unsigned grid = static_cast<unsigned>(need < grid_cap ? need : grid_cap);
