@@ -36,7 +36,7 @@ CU_SOURCES = [
 CPP_SOURCES = ["fb_capi.cpp", "fb_assembly.cpp", "fb_host.cpp", "fembatch_api.cpp", "fembatch_verify.cpp",
                "fembatch_bench.cpp"]
 CU_HOST_SOURCES = ["fb_tma.cpp"]  # host code that includes the kernel headers (nvcc)
-HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h", "fb_capi_util.h"]
+HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h", "fb_capi_util.h", "fb_asm_store.cuh"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "fembatch_b200.h"),
                   os.path.join(ROOT, "include", "fembatch_b200.hpp")]
 

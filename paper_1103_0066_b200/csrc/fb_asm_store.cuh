@@ -1,0 +1,54 @@
+// fb_asm_store.cuh -- write-out of a lane's contiguous CSR run in the
+// assembly kernels (fb_assemble.cu, fb_assemble_g.cu).  The runs of a warp's
+// lanes are far apart, so each lane's stores are separate L2 write requests:
+// scalar head up to FB_ASM_VB-byte alignment, then FB_ASM_VB-byte vector
+// stores (32: STG.E.ENL2.256, one full sector per request; 16: STG.128),
+// then a scalar tail.  next() yields the run's values in order.
+#pragma once
+
+#include <cstdint>
+
+#ifndef FB_ASM_VB
+#define FB_ASM_VB 32
+#endif
+
+namespace fbk {
+
+template <class S, int B>
+__device__ __forceinline__ void st_vec(S* p, const S (&q)[B / sizeof(S)])
+{
+  if constexpr (B == 32 && sizeof(S) == 4)
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(q[0]), "f"(q[1]),
+                 "f"(q[2]), "f"(q[3]), "f"(q[4]), "f"(q[5]), "f"(q[6]), "f"(q[7])
+                 : "memory");
+  else if constexpr (B == 32)
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(q[0]), "d"(q[1]), "d"(q[2]), "d"(q[3])
+                 : "memory");
+  else if constexpr (sizeof(S) == 4)
+    *reinterpret_cast<float4*>(p) = make_float4(q[0], q[1], q[2], q[3]);
+  else
+    *reinterpret_cast<double2*>(p) = make_double2(q[0], q[1]);
+}
+
+template <class S, class F>
+__device__ __forceinline__ void write_seq(S* base, int64_t len, F&& next)
+{
+  constexpr int W = FB_ASM_VB / static_cast<int>(sizeof(S));
+  int64_t head = (W - static_cast<int64_t>((reinterpret_cast<uintptr_t>(base) / sizeof(S)) % W)) % W;
+  head = head < len ? head : len;
+  int64_t p = 0;
+  for (; p < head; ++p)
+    base[p] = next();
+  for (; p + W <= len; p += W)
+  {
+    S q[W];
+#pragma unroll
+    for (int t = 0; t < W; ++t)
+      q[t] = next();
+    st_vec<S, FB_ASM_VB>(base + p, q);
+  }
+  for (; p < len; ++p)
+    base[p] = next();
+}
+
+}  // namespace fbk

@@ -20,6 +20,7 @@
 
 #include <cuda_runtime.h>
 
+#include "fb_asm_store.cuh"
 #include "fb_internal.h"
 
 namespace fbk {
@@ -110,27 +111,12 @@ __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
 #define FB_ASM_VECST 1
 #endif
 // base[p] = acc[p*T] for p < len (a lane's own shared-memory column:
-// conflict-free), with 16-byte vector stores between scalar head and tail.
-// The lanes' runs are far apart, so scalar stores would each be a separate
-// L2 write request; vectors cut them by 16 / sizeof(S).
+// conflict-free), with full-sector vector stores (fb_asm_store.cuh).
 template <class S, int T>
 __device__ __forceinline__ void write_run(S* base, int len, const S* acc)
 {
-  constexpr int W = 16 / static_cast<int>(sizeof(S));
-  int head = (W - static_cast<int>((reinterpret_cast<uintptr_t>(base) / sizeof(S)) % W)) % W;
-  head = head < len ? head : len;
   int p = 0;
-  for (; p < head; ++p)
-    base[p] = acc[p * T];
-  for (; p + W <= len; p += W)
-  {
-    if constexpr (W == 4)
-      *reinterpret_cast<float4*>(base + p) = make_float4(acc[p * T], acc[(p + 1) * T], acc[(p + 2) * T], acc[(p + 3) * T]);
-    else
-      *reinterpret_cast<double2*>(base + p) = make_double2(acc[p * T], acc[(p + 1) * T]);
-  }
-  for (; p < len; ++p)
-    base[p] = acc[p * T];
+  write_seq(base, len, [&]() { return acc[(p++) * T]; });
 }
 
 __host__ __device__ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_i(b, a % b); }

@@ -18,6 +18,7 @@
 
 #include <cuda_runtime.h>
 
+#include "fb_asm_store.cuh"
 #include "fb_kernels.cuh"
 
 namespace fbk {
@@ -147,15 +148,12 @@ __device__ __forceinline__ void select_row(const S (&vv)[NB * NB], int aa, S (&x
 #endif
 // Write-out of a vertex's CSR row block (nc rows x deg*nc entries,
 // contiguous, ci-major): entry (ci, k, cj) = acc[k] on the diagonal
-// (cj == ci), +0 elsewhere.  A lane's block is written with 16-byte vector
-// stores between scalar head and tail (a quarter of the L2 write requests of
-// scalar stores: the blocks of a warp's lanes are far apart, so per-lane
-// stores never coalesce).  acc reads are the lane's own shared-memory column
+// (cj == ci), +0 elsewhere, written with full-sector vector stores
+// (fb_asm_store.cuh).  acc reads are the lane's own shared-memory column
 // ([slot][thread]): conflict-free for any k.
 template <class S, int NC, int T>
 __device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
 {
-  constexpr int W = 16 / static_cast<int>(sizeof(S));
   const int64_t len = static_cast<int64_t>(deg) * NC * NC;
   int ci = 0, k = 0, cj = 0;
   auto next = [&]() -> S
@@ -172,35 +170,11 @@ __device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
     }
     return x;
   };
-  int64_t p = 0;
   if (FB_ASMG_VECST)
-  {
-    int64_t head = (W - static_cast<int64_t>((reinterpret_cast<uintptr_t>(base) / sizeof(S)) % W)) % W;
-    head = head < len ? head : len;
-    for (; p < head; ++p)
+    write_seq(base, len, next);
+  else
+    for (int64_t p = 0; p < len; ++p)
       base[p] = next();
-    for (; p + W <= len; p += W)
-    {
-      if constexpr (W == 4)
-      {
-        float4 q;
-        q.x = next();
-        q.y = next();
-        q.z = next();
-        q.w = next();
-        *reinterpret_cast<float4*>(base + p) = q;
-      }
-      else
-      {
-        double2 q;
-        q.x = next();
-        q.y = next();
-        *reinterpret_cast<double2*>(base + p) = q;
-      }
-    }
-  }
-  for (; p < len; ++p)
-    base[p] = next();
 }
 
 // A warp owns 32 consecutive vertices and all their rows.  Elasticity: the
