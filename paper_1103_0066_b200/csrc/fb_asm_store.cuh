@@ -1,16 +1,13 @@
 // fb_asm_store.cuh -- write-out of a lane's contiguous CSR run in the
 // assembly kernels (fb_assemble.cu, fb_assemble_g.cu).  The runs of a warp's
 // lanes are far apart, so each lane's stores are separate L2 write requests:
-// scalar head up to FB_ASM_VB-byte alignment, then FB_ASM_VB-byte vector
-// stores (32: STG.E.ENL2.256, one full sector per request; 16: STG.128),
-// then a scalar tail.  next() yields the run's values in order.
+// scalar head up to B-byte alignment, then B-byte vector stores (32:
+// STG.E.ENL2.256, one full sector per request; 16: STG.128), then a scalar
+// tail.  next() yields the run's values in order.
 #pragma once
 
 #include <cstdint>
 
-#ifndef FB_ASM_VB
-#define FB_ASM_VB 32
-#endif
 
 namespace fbk {
 
@@ -30,10 +27,10 @@ __device__ __forceinline__ void st_vec(S* p, const S (&q)[B / sizeof(S)])
     *reinterpret_cast<double2*>(p) = make_double2(q[0], q[1]);
 }
 
-template <class S, class F>
+template <class S, int B, class F>
 __device__ __forceinline__ void write_seq(S* base, int64_t len, F&& next)
 {
-  constexpr int W = FB_ASM_VB / static_cast<int>(sizeof(S));
+  constexpr int W = B / static_cast<int>(sizeof(S));
   int64_t head = (W - static_cast<int64_t>((reinterpret_cast<uintptr_t>(base) / sizeof(S)) % W)) % W;
   head = head < len ? head : len;
   int64_t p = 0;
@@ -45,7 +42,7 @@ __device__ __forceinline__ void write_seq(S* base, int64_t len, F&& next)
 #pragma unroll
     for (int t = 0; t < W; ++t)
       q[t] = next();
-    st_vec<S, FB_ASM_VB>(base + p, q);
+    st_vec<S, B>(base + p, q);
   }
   for (; p < len; ++p)
     base[p] = next();

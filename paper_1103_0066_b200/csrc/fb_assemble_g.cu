@@ -171,7 +171,7 @@ __device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
     return x;
   };
   if (FB_ASMG_VECST)
-    write_seq(base, len, next);
+    write_seq<S, 32>(base, len, next);  // A/B: 16-byte stores 0.56 -> 0.43 ms (3D-E f32)
   else
     for (int64_t p = 0; p < len; ++p)
       base[p] = next();
