@@ -177,6 +177,58 @@ __device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
       base[p] = next();
 }
 
+#ifndef FB_ASMG_ROW
+#define FB_ASMG_ROW 1
+#endif
+// Row a != 0 (runtime) of contract_sparse<SYM = false>: on the P1 pattern
+// only mu = a-1 contributes, so the row needs G's row a-1 (dim scalars)
+// alone.  Same terms, same (c, mu, nu) order, same operations as
+// contract_sparse, hence the same bits.
+template <class S, int DIM, int OP, int MODE, bool UNI>
+__device__ __forceinline__ void contract_row(const S (&gr)[DIM], const S (&w)[DIM + 1], const KP<S, DIM, OP>& kp,
+                                             int a, S (&x)[DIM + 1])
+{
+  using Sh = Shape<DIM, OP>;
+  using A = Ar<S, MODE>;
+  constexpr int NB = DIM + 1, NC = Sh::NC, DD = Sh::DD;
+  S m[UNI ? NC * DIM : 1];
+  if (UNI)
+  {
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int nu = 0; nu < DIM; ++nu)
+        m[UNI ? c * DIM + nu : 0] = OP == kWeighted ? A::mul(A::mul(w[c], gr[nu]), kp.k[c]) : A::mul(gr[nu], kp.k[c]);
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+  {
+    S acc = S(0);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int nu = 0; nu < DIM; ++nu)
+      {
+        if (b != 0 && nu != b - 1)
+          continue;
+        if (UNI)
+        {
+          const S p = m[UNI ? c * DIM + nu : 0];
+          acc = A::add(acc, b == 0 ? -p : p);  // sigma_ab = -1 iff b == 0 (a != 0)
+        }
+        else
+        {
+          const S kv = kp.k[((a * NB + b) * NC + c) * DD + (a - 1) * DIM + nu];
+          if (OP == kWeighted)
+            acc = A::mac(acc, A::mul(w[c], gr[nu]), kv);
+          else
+            acc = A::mac(acc, gr[nu], kv);
+        }
+      }
+    x[b] = acc;
+  }
+}
+
 // A warp owns 32 consecutive vertices and all their rows.  Elasticity: the
 // element matrix is block diagonal with nc copies of the Laplacian-like
 // block, so the nc diagonal component blocks of a CSR row block receive the
@@ -184,7 +236,7 @@ __device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
 // to the nc diagonal entries; the off-diagonal entries are written as +0.
 template <class S, int DIM, int OP, int MODE, bool UNI>
 __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
-    fb_assemble_g_kernel(const AsmArgs a, const KP<S, DIM, OP> kp)
+    fb_assemble_g_kernel(const AsmArgs a, const __grid_constant__ KP<S, DIM, OP> kp)
 {
   using G = GShape<S, DIM, OP>;
   constexpr int NB = DIM + 1, NC = G::NC, DD = DIM * DIM;
@@ -234,8 +286,18 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
       for (int u = 0; u < U; ++u)
       {
         const int64_t e = pk[u] != kPadG ? (pk[u] >> 2) : 0;
+        const int aa = static_cast<int>(pk[u] & 3u);
         if (pk[u] != kPadG)
-          load_g<S, DD>(gin, e, a.g_len, ge[u]);
+        {
+          if (!FB_ASMG_ROW || aa == 0)
+            load_g<S, DD>(gin, e, a.g_len, ge[u]);
+          else  // row a-1 of G only
+          {
+#pragma unroll
+            for (int nu = 0; nu < DIM; ++nu)
+              ge[u][nu] = __ldg(gin + e * DD + (aa - 1) * DIM + nu);
+          }
+        }
 #pragma unroll
         for (int c = 0; c <= DIM; ++c)
           we[u][c] = OP == kWeighted && pk[u] != kPadG ? static_cast<S>(__ldg(a.coeffs + e * (DIM + 1) + c)) : S(0);
@@ -245,9 +307,30 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
       for (int u = 0; u < U; ++u)
         if (pk[u] != kPadG)
         {
-          S vv[NB * NB], x[NB];
-          contract_sparse<S, DIM, OP, MODE, false, UNI>(ge[u], we[u], kp, vv);
-          select_row<S, NB>(vv, static_cast<int>(pk[u] & 3u), x);
+          const int aa = static_cast<int>(pk[u] & 3u);
+          S x[NB];
+          if (!FB_ASMG_ROW)
+          {
+            S vv[NB * NB];
+            contract_sparse<S, DIM, OP, MODE, false, UNI>(ge[u], we[u], kp, vv);
+            select_row<S, NB>(vv, aa, x);
+          }
+          else if (aa == 0)
+          {
+            S vv[NB * NB];
+            contract_sparse<S, DIM, OP, MODE, false, UNI>(ge[u], we[u], kp, vv);
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+              x[b] = vv[b];
+          }
+          else
+          {
+            S gr[DIM];
+#pragma unroll
+            for (int nu = 0; nu < DIM; ++nu)
+              gr[nu] = ge[u][nu];
+            contract_row<S, DIM, OP, MODE, UNI>(gr, we[u], kp, aa, x);
+          }
 #pragma unroll
           for (int b = 0; b < NB; ++b)
           {
