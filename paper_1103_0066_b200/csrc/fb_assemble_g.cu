@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
   using G = GShape<S, DIM, OP>;
   constexpr int NB = DIM + 1, NC = G::NC, DD = DIM * DIM;
   constexpr int T = 32 * G::WARPS, SLOTS = G::SLOTS, U = G::U;
+  // row-only contraction for a != 0: 3D (A/B: 3D-E f32 0.43 -> 0.38 ms, f64
+  // 0.74 -> 0.61, 3D-L f32 0.65 -> 0.53); 2D loses ~5 % (2D-E 0.033 -> 0.035)
+  constexpr bool ROWP = FB_ASMG_ROW && DIM == 3;
   __shared__ S acc_s[SLOTS * T];
   S* acc = acc_s + threadIdx.x;
   S* vals = static_cast<S*>(a.values);
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
         const int aa = static_cast<int>(pk[u] & 3u);
         if (pk[u] != kPadG)
         {
-          if (!FB_ASMG_ROW || aa == 0)
+          if (!ROWP || aa == 0)
             load_g<S, DD>(gin, e, a.g_len, ge[u]);
           else  // row a-1 of G only
           {
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
         {
           const int aa = static_cast<int>(pk[u] & 3u);
           S x[NB];
-          if (!FB_ASMG_ROW)
+          if (!ROWP)
           {
             S vv[NB * NB];
             contract_sparse<S, DIM, OP, MODE, false, UNI>(ge[u], we[u], kp, vv);
