@@ -220,6 +220,10 @@ def _packed_case(var, op, dim, v, c, prec, bs, offset=0):
     host = plan.assemble_packed(var, g.cpu().numpy(), w)
     assert host.tobytes() == want.cpu().numpy().tobytes()
     assert torch.equal(plan.assemble_packed(var, g, dw), want)
+    # mixed residency: host G and coefficients, device values
+    mixed = torch.full_like(want, float("nan"))
+    plan.assemble_packed(var, g.cpu().numpy(), w, values=mixed)
+    assert torch.equal(mixed, want)
     return want, got
 
 
