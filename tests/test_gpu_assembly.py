@@ -293,3 +293,25 @@ def test_packed_assembly_validation(restatement):
     assert dvar.path == 2
     with pytest.raises(_lib.InvalidArgument, match="P1 sparsity"):
         plan.assemble_packed_async(dvar, g, vals)
+
+
+@pytest.mark.parametrize("op,dim", [("laplacian", 2), ("elasticity", 3), ("weighted-laplacian", 3)])
+def test_assembly_of_an_empty_mesh(op, dim):
+    import torch
+
+    cells = np.zeros(0, dtype=np.int32)
+    for c in (cells, torch.from_numpy(cells).cuda()):
+        plan = fb.AssemblyPlan(op, dim, c, 5)
+        nc = dim if op == "elasticity" else 1
+        assert plan.rows == 5 * nc and plan.nnz == 0
+        rp, ci = plan.pattern()
+        assert rp.tolist() == [0] * (5 * nc + 1) and ci.size == 0
+        var = fb.make_variant(op, dim, "f64", element_batch_size=4)
+        assert plan.assemble(var, np.zeros(0)).size == 0
+        coeffs = np.zeros(0) if op == "weighted-laplacian" else None
+        assert plan.assemble_packed(var, np.zeros(0), coeffs).size == 0
+        vals = torch.empty(0, dtype=torch.float64, device="cuda")
+        plan.assemble_packed_async(var, torch.empty(0, dtype=torch.float64, device="cuda"), vals,
+                                   torch.empty(0, dtype=torch.float64, device="cuda") if coeffs is not None else None,
+                                   torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
