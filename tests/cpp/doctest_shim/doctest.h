@@ -118,6 +118,7 @@ inline int run_all()
       std::printf("%s:%d: TEST_CASE \"%s\" threw an unknown exception\n", c.file, c.line, c.name);
     }
     failed_cases += state().case_failed ? 1 : 0;
+    std::printf("[doctest-shim] %s: %s\n", state().case_failed ? "FAIL" : "PASS", c.name);
   }
   std::printf("[doctest-shim] test cases: %zu | %zu passed | %d failed\n", cases().size(),
               cases().size() - static_cast<size_t>(failed_cases), failed_cases);

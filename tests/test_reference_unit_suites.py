@@ -48,3 +48,34 @@ def test_host_suites_pass_on_the_b200_api(unit):
 def test_all_reference_suites_pass_on_the_gpu_engine(unit):
     total, passed, r = run_suite(f"unit_{unit}_b200")
     assert total == CASES[unit] and passed == total and r.returncode == 0, r.stdout[-3000:]
+
+
+# Host-only cases of the oracle and bench suites run on CPU against this
+# repo's own verification / bench-record modules (csrc/fembatch_verify.cpp,
+# fembatch_bench.cpp); the cases that integrate on the GPU run in the gpu test
+# above.
+HOST_CASES = {
+    "oracle": ["direct assembly reproduces the classical reference stiffness",
+               "direct assembly is invariant under uniform scaling in 2D",
+               "direct weighted assembly with unit weights matches the Laplacian",
+               "direct elasticity assembly pairs components diagonally",
+               "direct assembly produces symmetric singular stiffness matrices",
+               "direct assembly validates input sizes"],
+    "bench": ["the default coefficient field samples 1 + x0 at cell vertices",
+              "the store checksum ignores padding slots entirely",
+              "default tolerances are pinned per precision",
+              "invalid configurations yield status rows instead of throws",
+              "sweeps mark non-dividing concurrency as invalid rows",
+              "CSV output round-trips records exactly",
+              "the CSV header is stable",
+              "the CSV reader rejects malformed input",
+              "JSON output parses back with the same values"],
+}
+
+
+@pytest.mark.parametrize("unit", sorted(HOST_CASES))
+def test_host_cases_of_verify_and_bench_suites_on_the_b200_api(unit):
+    _, _, r = run_suite(f"unit_{unit}_b200")
+    status = dict(reversed(m) for m in re.findall(r"\[doctest-shim\] (PASS|FAIL): (.*)", r.stdout))
+    for name in HOST_CASES[unit]:
+        assert status.get(name) == "PASS", (name, r.stdout[-3000:])
