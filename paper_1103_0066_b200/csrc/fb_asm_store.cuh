@@ -9,14 +9,7 @@
 #include <cstdint>
 
 
-#ifndef FB_ASM_CS
-#define FB_ASM_CS 0  // streaming (.cs) hint on the CSR value stores (A/B knob)
-#endif
-#if FB_ASM_CS
-#define FB_ASM_STOP ".cs"
-#else
-#define FB_ASM_STOP ""
-#endif
+// (A/B: a streaming .cs hint on these stores changes nothing measurable.)
 
 namespace fbk {
 
@@ -24,20 +17,20 @@ template <class S, int B>
 __device__ __forceinline__ void st_vec(S* p, const S (&q)[B / sizeof(S)])
 {
   if constexpr (B == 32 && sizeof(S) == 4)
-    asm volatile("st.global" FB_ASM_STOP ".v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(q[0]),
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(q[0]),
                  "f"(q[1]),
                  "f"(q[2]), "f"(q[3]), "f"(q[4]), "f"(q[5]), "f"(q[6]), "f"(q[7])
                  : "memory");
   else if constexpr (B == 32)
-    asm volatile("st.global" FB_ASM_STOP ".v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(q[0]), "d"(q[1]), "d"(q[2]),
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(q[0]), "d"(q[1]), "d"(q[2]),
                  "d"(q[3])
                  : "memory");
   else if constexpr (sizeof(S) == 4)
-    asm volatile("st.global" FB_ASM_STOP ".v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(q[0]), "f"(q[1]), "f"(q[2]),
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(q[0]), "f"(q[1]), "f"(q[2]),
                  "f"(q[3])
                  : "memory");
   else
-    asm volatile("st.global" FB_ASM_STOP ".v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(q[0]), "d"(q[1]) : "memory");
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(q[0]), "d"(q[1]) : "memory");
 }
 
 template <class S, int B, class F>
