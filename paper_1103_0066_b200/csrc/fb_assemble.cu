@@ -74,6 +74,9 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 
 // N contiguous scalars from p, whose address is a multiple of A bytes
 // (A = 16, 8 or 4): the widest aligned vector loads.
+#ifndef FB_ASM_EVL
+#define FB_ASM_EVL 0  // A/B knob
+#endif
 template <class S, int N, int A>
 __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
 {
@@ -92,9 +95,21 @@ __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
     }
     else if constexpr (W == 2 && sizeof(S) == 8)
     {
+#if FB_ASM_EVL
+      // element rows kept in L2 (evict_last): an element's rows are re-read
+      // when its other vertices' groups come round
+      double x, y;
+      asm("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                   "ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
+                   : "=d"(x), "=d"(y)
+                   : "l"(p + t));
+      r[t] = x;
+      r[t + 1] = y;
+#else
       const double2 q = __ldg(reinterpret_cast<const double2*>(p + t));
       r[t] = q.x;
       r[t + 1] = q.y;
+#endif
     }
     else if constexpr (W == 2)
     {
