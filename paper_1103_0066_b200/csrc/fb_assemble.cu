@@ -77,6 +77,27 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 #ifndef FB_ASM_EVL
 #define FB_ASM_EVL 0  // A/B knob
 #endif
+#ifndef FB_ASM_EVF
+#define FB_ASM_EVF 0  // A/B knob
+#endif
+// scalar CSR value store; with FB_ASM_EVF under an L2 evict_first policy so
+// the streaming output does not push re-read element rows out of L2
+template <class S>
+__device__ __forceinline__ void st_evict_first(S* p, S v)
+{
+#if FB_ASM_EVF
+  if constexpr (sizeof(S) == 8)
+    asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                 "st.global.L2::cache_hint.f64 [%0], %1, pol;\n\t}" ::"l"(p), "d"(v)
+                 : "memory");
+  else
+    asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                 "st.global.L2::cache_hint.f32 [%0], %1, pol;\n\t}" ::"l"(p), "f"(v)
+                 : "memory");
+#else
+  *p = v;
+#endif
+}
 template <class S, int N, int A>
 __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
 {
@@ -331,7 +352,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
       else
         for (int k = 0; k < deg; ++k)
           for (int c = 0; c < NCW; ++c)
-            vals[row + k * NC + c] = acc[(k * NCW + c) * T];
+            st_evict_first(vals + row + k * NC + c, acc[(k * NCW + c) * T]);
     }
     cur = nxt;
   }
