@@ -33,6 +33,37 @@ __device__ __forceinline__ void st_vec(S* p, const S (&q)[B / sizeof(S)])
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(q[0]), "d"(q[1]) : "memory");
 }
 
+// Read-only loads under an L2 evict_last policy: element rows / G entries
+// that other vertices' groups re-read later stay in L2 ahead of the
+// streaming plan and CSR traffic.
+#define FB_EVL_POLICY "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+__device__ __forceinline__ float ld_el(const float* p)
+{
+  float x;
+  asm(FB_EVL_POLICY "ld.global.nc.L2::cache_hint.f32 %0, [%1], pol;\n\t}" : "=f"(x) : "l"(p));
+  return x;
+}
+__device__ __forceinline__ double ld_el(const double* p)
+{
+  double x;
+  asm(FB_EVL_POLICY "ld.global.nc.L2::cache_hint.f64 %0, [%1], pol;\n\t}" : "=d"(x) : "l"(p));
+  return x;
+}
+__device__ __forceinline__ float4 ld_el(const float4* p)
+{
+  float4 q;
+  asm(FB_EVL_POLICY "ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+      : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+      : "l"(p));
+  return q;
+}
+__device__ __forceinline__ double2 ld_el(const double2* p)
+{
+  double2 q;
+  asm(FB_EVL_POLICY "ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}" : "=d"(q.x), "=d"(q.y) : "l"(p));
+  return q;
+}
+
 template <class S, int B, class F>
 __device__ __forceinline__ void write_seq(S* base, int64_t len, F&& next)
 {

@@ -78,7 +78,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 #define FB_ASM_EVL 1  // A/B: 3D-E f64 4.93 -> 4.67 ms, neutral elsewhere
 #endif
 #ifndef FB_ASM_EVL32
-#define FB_ASM_EVL32 0  // the same for FP32 rows (A/B knob)
+#define FB_ASM_EVL32 1  // FP32 rows too (A/B: 3D-E f32 1.62 -> 1.59 ms, 3D-L 0.403 -> 0.398)
 #endif
 template <class S, int N, int A>
 __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
@@ -90,41 +90,19 @@ __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
   {
     if constexpr (W == 4)
     {
-#if FB_ASM_EVL32
-      float x, y, z, w;
-      asm("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-          "ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
-          : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
-          : "l"(p + t));
-      r[t] = x;
-      r[t + 1] = y;
-      r[t + 2] = z;
-      r[t + 3] = w;
-#else
-      const float4 q = __ldg(reinterpret_cast<const float4*>(p + t));
+      const float4 q = FB_ASM_EVL32 ? ld_el(reinterpret_cast<const float4*>(p + t))
+                                   : __ldg(reinterpret_cast<const float4*>(p + t));
       r[t] = q.x;
       r[t + 1] = q.y;
       r[t + 2] = q.z;
       r[t + 3] = q.w;
-#endif
     }
     else if constexpr (W == 2 && sizeof(S) == 8)
     {
-#if FB_ASM_EVL
-      // element rows kept in L2 (evict_last): an element's rows are re-read
-      // when its other vertices' groups come round
-      double x, y;
-      asm("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-                   "ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
-                   : "=d"(x), "=d"(y)
-                   : "l"(p + t));
-      r[t] = x;
-      r[t + 1] = y;
-#else
-      const double2 q = __ldg(reinterpret_cast<const double2*>(p + t));
+      const double2 q = FB_ASM_EVL ? ld_el(reinterpret_cast<const double2*>(p + t))
+                                  : __ldg(reinterpret_cast<const double2*>(p + t));
       r[t] = q.x;
       r[t + 1] = q.y;
-#endif
     }
     else if constexpr (W == 2)
     {

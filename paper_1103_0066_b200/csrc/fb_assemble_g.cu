@@ -32,6 +32,17 @@ constexpr uint32_t kPadG = 0xffffffffu;
 #ifndef FB_ASMG_U
 #define FB_ASMG_U 4
 #endif
+#ifndef FB_ASMG_EVL
+#define FB_ASMG_EVL 0  // G loads under an L2 evict_last policy (A/B knob)
+#endif
+template <class T>
+__device__ __forceinline__ T ldg_g(const T* p)
+{
+  if constexpr (FB_ASMG_EVL)
+    return ld_el(p);
+  else
+    return __ldg(p);
+}
 #ifndef FB_ASMG_VEC
 #define FB_ASMG_VEC 1
 #endif
@@ -67,7 +78,7 @@ __device__ __forceinline__ void load_g(const S* gin, int64_t e, int64_t ng, S (&
   {
 #pragma unroll
     for (int t = 0; t < DD; ++t)
-      g[t] = __ldg(gin + first + t);
+      g[t] = ldg_g(gin + first + t);
     return;
   }
   if constexpr (DD % W == 0)
@@ -78,12 +89,12 @@ __device__ __forceinline__ void load_g(const S* gin, int64_t e, int64_t ng, S (&
     {
       if constexpr (W == 4)
       {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(gin + first + t));
+        const float4 q = ldg_g(reinterpret_cast<const float4*>(gin + first + t));
         g[t] = q.x, g[t + 1] = q.y, g[t + 2] = q.z, g[t + 3] = q.w;
       }
       else
       {
-        const double2 q = __ldg(reinterpret_cast<const double2*>(gin + first + t));
+        const double2 q = ldg_g(reinterpret_cast<const double2*>(gin + first + t));
         g[t] = q.x, g[t + 1] = q.y;
       }
     }
@@ -97,7 +108,7 @@ __device__ __forceinline__ void load_g(const S* gin, int64_t e, int64_t ng, S (&
     {
 #pragma unroll
       for (int t = 0; t < DD; ++t)
-        g[t] = __ldg(gin + first + t);
+        g[t] = ldg_g(gin + first + t);
       return;
     }
     S c[NW * W];
@@ -106,12 +117,12 @@ __device__ __forceinline__ void load_g(const S* gin, int64_t e, int64_t ng, S (&
     {
       if constexpr (W == 4)
       {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(gin + w0) + k);
+        const float4 q = ldg_g(reinterpret_cast<const float4*>(gin + w0) + k);
         c[4 * k] = q.x, c[4 * k + 1] = q.y, c[4 * k + 2] = q.z, c[4 * k + 3] = q.w;
       }
       else
       {
-        const double2 q = __ldg(reinterpret_cast<const double2*>(gin + w0) + k);
+        const double2 q = ldg_g(reinterpret_cast<const double2*>(gin + w0) + k);
         c[2 * k] = q.x, c[2 * k + 1] = q.y;
       }
     }
@@ -298,7 +309,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
           {
 #pragma unroll
             for (int nu = 0; nu < DIM; ++nu)
-              ge[u][nu] = __ldg(gin + e * DD + (aa - 1) * DIM + nu);
+              ge[u][nu] = ldg_g(gin + e * DD + (aa - 1) * DIM + nu);
           }
         }
 #pragma unroll
