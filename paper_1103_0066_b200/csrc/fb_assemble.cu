@@ -43,6 +43,9 @@ namespace {
 #ifndef FB_ASM_NCW2
 #define FB_ASM_NCW2 2  // 2D elasticity: a warp reads the whole element row (A/B: 1 is slower)
 #endif
+#ifndef FB_ASM_WARPS_NCW
+#define FB_ASM_WARPS_NCW 2  // warps per CTA when a warp reads several column components
+#endif
 #ifndef FB_ASM_NCW3D64
 #define FB_ASM_NCW3D64 1  // 3D elasticity FP64
 #endif
@@ -52,7 +55,7 @@ namespace {
 template <class S, int DIM, int NC>
 struct AsmShape {
   static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : (NC == 3 ? FB_ASM_NCW3D64 : 1));
-  static constexpr int WARPS = NCW == 1 ? 4 : 2;
+  static constexpr int WARPS = NCW == 1 ? 4 : FB_ASM_WARPS_NCW;
   static constexpr int SLOTS = NCW == 1 ? 32 : 24;
   static constexpr int U = DIM == 2 ? FB_ASM_U2D : (NCW == 1 ? FB_ASM_U : 4);
   // prefetch the next chunk's plan entries (registers: 3D elasticity FP64,
