@@ -262,14 +262,6 @@ int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, in
 int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* store,
                       int64_t store_len, void* values, int64_t nnz, int flags, void* stream,
                       fb_error* err);
-/* Optional schedule: process the plan's 32-vertex groups along a Morton
- * curve of their centroids (vertices: num_vertices*dim doubles, host or
- * device) so that groups sharing elements run close together and the element
- * data they re-read is still in L2.  Values are bitwise unchanged (each CSR
- * entry's sum order is per vertex).  vertices = NULL restores ascending
- * order.  Not thread-safe against concurrent fb_assemble* on the same plan. */
-int fb_assembly_order_groups(fb_assembly* a, const double* vertices, int64_t num_vertices,
-                             fb_error* err);
 /* Assembly straight from packed geometry (the fb_integrate_batches input:
  * g = num_elements*dim^2 scalars in engine precision, PackedGeometry layout;
  * coeffs = num_elements*(dim+1) doubles for the weighted Laplacian, else

@@ -70,7 +70,6 @@ SIGNATURES = {
     "fb_assemble": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _E]),
     "fb_assemble_async": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _E]),
     "fb_assemble_packed_async": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _E]),
-    "fb_assembly_order_groups": (_i32, [_vp, _vp, _i64, _E]),
     "fb_assemble_packed": (_i32, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _E]),
 }
 

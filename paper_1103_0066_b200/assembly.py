@@ -63,17 +63,6 @@ class AssemblyPlan:
                                                   col_idx.ctypes.data, col_idx.size, C.byref(err)), err)
         return row_ptr, col_idx
 
-    def order_groups(self, vertices=None):
-        """Schedule the vertex groups along a Morton curve of their centroids
-        (better L2 reuse of element data; values bitwise unchanged).
-        ``None`` restores ascending order."""
-        if vertices is not None:
-            vertices = _as(vertices, np.float64)
-        err = L.fb_error()
-        L.raise_for(self._lib.fb_assembly_order_groups(self._h, _ptr(vertices),
-                                                       _numel(vertices) // self.dim if vertices is not None else 0,
-                                                       C.byref(err)), err)
-
     def assemble(self, variant: KernelVariant, store, values=None, device: int = 0, symmetric: bool = False):
         """CSR values (engine precision) of the element matrices in ``store``.
 

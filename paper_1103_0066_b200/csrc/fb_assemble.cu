@@ -181,8 +181,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   auto load_desc = [&](int64_t w)
   {
     Desc d;
-    const int64_t gt = w / (NC * NWC);
-    const int64_t g = a.gorder ? static_cast<int64_t>(__ldg(a.gorder + gt)) : gt;
+    const int64_t g = w / (NC * NWC);
     const int64_t v = g * 32 + lane;
     if (v < a.nv)
     {
@@ -218,8 +217,8 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
     Desc nxt;
     if (w + wstride < nwarps)
       nxt = load_desc(w + wstride);
-    const int64_t gt = w / (NC * NWC);
-    const int sub = static_cast<int>(w - gt * (NC * NWC));
+    const int64_t g = w / (NC * NWC);
+    const int sub = static_cast<int>(w - g * (NC * NWC));
     const int ci = sub / NWC, cj0 = (sub % NWC) * NCW;
     const int64_t r0 = cur.r0;
     const int deg = static_cast<int>(cur.r1 - cur.r0);

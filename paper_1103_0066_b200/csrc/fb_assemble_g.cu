@@ -261,10 +261,9 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
   const S* gin = static_cast<const S*>(a.g_in);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (a.nv + 31) / 32;
-  for (int64_t gt = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); gt < nwarps;
-       gt += static_cast<int64_t>(gridDim.x) * (T / 32))
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); g < nwarps;
+       g += static_cast<int64_t>(gridDim.x) * (T / 32))
   {
-    const int64_t g = a.gorder ? static_cast<int64_t>(__ldg(a.gorder + gt)) : gt;
     const int64_t v = g * 32 + lane;
     const bool live = v < a.nv;
     const int64_t r0 = live ? __ldg(a.nbr_ptr + v) : 0;

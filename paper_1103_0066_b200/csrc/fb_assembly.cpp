@@ -34,7 +34,6 @@ struct DevPlan {
   uint32_t* spos = nullptr;
   int64_t* nbr_ptr = nullptr;
   int32_t* nbr = nullptr;  // only on the device that built the plan
-  int32_t* gorder = nullptr;  // group processing order (fb_assembly_order_groups)
 };
 
 }  // namespace
@@ -50,7 +49,6 @@ struct fb_assembly {
   std::vector<int64_t> goff;
   std::vector<uint32_t> spk, spos;
   int64_t total_nbr = 0;  // sum of vertex degrees
-  std::vector<int32_t> gorder;  // group processing order; empty = ascending
   int home = -1;          // device that built the plan (host arrays filled lazily), -1 = host-built
   mutable std::mutex mu;
   mutable std::map<int, DevPlan> dev;
@@ -68,7 +66,6 @@ struct fb_assembly {
       cudaFree(p.spos);
       cudaFree(p.nbr_ptr);
       cudaFree(p.nbr);
-      cudaFree(p.gorder);
     }
     cudaSetDevice(cur);
   }
@@ -291,66 +288,15 @@ const DevPlan& plan_on(const fb_assembly& A, int dev)
 {
   std::lock_guard<std::mutex> lock(A.mu);
   auto it = A.dev.find(dev);
-  if (it == A.dev.end())
-  {
-    ensure_host(A);
-    DevPlan p;
-    p.goff = upload(A.goff);
-    p.spk = upload(A.spk);
-    p.spos = upload(A.spos);
-    p.nbr_ptr = upload(A.nbr_ptr);
-    it = A.dev.emplace(dev, p).first;
-  }
-  if (!A.gorder.empty() && !it->second.gorder)
-    it->second.gorder = upload(A.gorder);
-  return it->second;
-}
-
-// Groups of 32 vertices ordered along a Morton (Z-order) curve of their
-// centroids: groups that share elements are scheduled close together, so an
-// element's data is still in L2 when its other vertices' groups read it.
-std::vector<int32_t> morton_group_order(const fb_assembly& A, const double* x)
-{
-  const int dim = A.dim;
-  const int64_t ng = (A.nv + 31) / 32;
-  std::vector<double> c(static_cast<size_t>(ng) * dim, 0.0);
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int64_t g = 0; g < ng; ++g)
-  {
-    const int64_t v0 = g * 32, v1 = std::min<int64_t>(A.nv, v0 + 32);
-    for (int d = 0; d < dim; ++d)
-    {
-      double s = 0.0;
-      for (int64_t v = v0; v < v1; ++v)
-        s += x[v * dim + d];
-      const double m = s / static_cast<double>(v1 - v0);
-      c[static_cast<size_t>(g) * dim + d] = m;
-      lo[d] = std::min(lo[d], m);
-      hi[d] = std::max(hi[d], m);
-    }
-  }
-  const int bits = dim == 2 ? 31 : 21;
-  const double top = static_cast<double>((uint64_t(1) << bits) - 1);
-  std::vector<std::pair<uint64_t, int32_t>> key(static_cast<size_t>(ng));
-  for (int64_t g = 0; g < ng; ++g)
-  {
-    uint64_t k = 0;
-    for (int d = 0; d < dim; ++d)
-    {
-      const double span = hi[d] > lo[d] ? hi[d] - lo[d] : 1.0;
-      double t = (c[static_cast<size_t>(g) * dim + d] - lo[d]) / span * top;
-      t = t != t ? 0.0 : std::min(std::max(t, 0.0), top);  // NaN / out of range -> clamp
-      const uint64_t q = static_cast<uint64_t>(t);
-      for (int b = 0; b < bits; ++b)
-        k |= ((q >> b) & 1u) << (b * dim + d);
-    }
-    key[static_cast<size_t>(g)] = {k, static_cast<int32_t>(g)};
-  }
-  std::sort(key.begin(), key.end());
-  std::vector<int32_t> order(static_cast<size_t>(ng));
-  for (int64_t g = 0; g < ng; ++g)
-    order[static_cast<size_t>(g)] = key[static_cast<size_t>(g)].second;
-  return order;
+  if (it != A.dev.end())
+    return it->second;
+  ensure_host(A);
+  DevPlan p;
+  p.goff = upload(A.goff);
+  p.spk = upload(A.spk);
+  p.spos = upload(A.spos);
+  p.nbr_ptr = upload(A.nbr_ptr);
+  return A.dev.emplace(dev, p).first->second;
 }
 
 void check_pair(const fb_assembly* a, const fb_variant* v, int64_t store_len, int64_t nnz)
@@ -384,7 +330,6 @@ void launch_on(const fb_assembly& A, const fb_variant& v, const void* store, voi
   g.spk = p.spk;
   g.spos = p.spos;
   g.nbr_ptr = p.nbr_ptr;
-  g.gorder = p.gorder;
   g.store = store;
   g.values = values;
   g.nv = A.nv;
@@ -426,7 +371,6 @@ void launch_packed_on(const fb_assembly& A, const fb_variant& v, const void* g, 
   ga.spk = p.spk;
   ga.spos = p.spos;
   ga.nbr_ptr = p.nbr_ptr;
-  ga.gorder = p.gorder;
   ga.values = values;
   ga.nv = A.nv;
   // vector loads need a 16-byte aligned G; else the kernel reads it scalar-wise
@@ -520,50 +464,6 @@ int fb_assemble_async(const fb_assembly* a, const fb_variant* v, const void* sto
                    int dev = 0;
                    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
                    launch_on(*a, *v, store, values, flags, dev, static_cast<cudaStream_t>(stream));
-                 });
-}
-
-int fb_assembly_order_groups(fb_assembly* a, const double* vertices, int64_t num_vertices, fb_error* err)
-{
-  return guarded(err,
-                 [&]
-                 {
-                   if (!a)
-                     invalid("null assembly plan");
-                   std::vector<int32_t> order;
-                   if (vertices)
-                   {
-                     if (num_vertices != a->nv)
-                       invalid("vertex count differs from the plan's");
-                     if (a->nv > 0)
-                     {
-                       std::vector<double> host;
-                       const double* x = vertices;
-                       if (pointer_device(vertices) >= 0)
-                       {
-                         host.resize(static_cast<size_t>(a->nv) * a->dim);
-                         cuda_check(cudaMemcpy(host.data(), vertices, host.size() * sizeof(double),
-                                               cudaMemcpyDefault),
-                                    "cudaMemcpy vertices");
-                         x = host.data();
-                       }
-                       order = morton_group_order(*a, x);
-                     }
-                   }
-                   std::lock_guard<std::mutex> lock(a->mu);
-                   a->gorder = std::move(order);
-                   int cur = 0;
-                   cudaGetDevice(&cur);
-                   for (auto& [d, p] : a->dev)  // re-uploaded on next use
-                   {
-                     if (p.gorder)
-                     {
-                       cudaSetDevice(d);
-                       cudaFree(p.gorder);
-                       p.gorder = nullptr;
-                     }
-                   }
-                   cudaSetDevice(cur);
                  });
 }
 

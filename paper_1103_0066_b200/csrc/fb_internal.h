@@ -88,9 +88,6 @@ struct AsmArgs {
   const void* g_in = nullptr;
   const double* coeffs = nullptr;   // weighted form: ne*(dim+1) nodal coefficients
   int64_t g_len = 0;                // scalars readable at g_in (16-byte aligned)
-  // optional processing order of the 32-vertex groups (a permutation; null =
-  // ascending): only the schedule changes, every value is bitwise the same
-  const int32_t* gorder = nullptr;
 };
 cudaError_t launch_assemble(int dim, int nc, int prec, const AsmArgs&, cudaStream_t);
 cudaError_t launch_assemble_g(const LaunchSpec& s, const AsmArgs&, const KParamBlob&, cudaStream_t);

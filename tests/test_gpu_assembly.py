@@ -315,34 +315,3 @@ def test_assembly_of_an_empty_mesh(op, dim):
                                    torch.empty(0, dtype=torch.float64, device="cuda") if coeffs is not None else None,
                                    torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
-
-
-@pytest.mark.parametrize("op,dim", [("laplacian", 3), ("elasticity", 3), ("elasticity", 2), ("weighted-laplacian", 2)])
-@pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_group_order_changes_schedule_not_values(op, dim, prec):
-    import torch
-
-    v, c = fb.structured_mesh(dim, 9 if dim == 3 else 40, 0.15, 3)
-    nv, ne = v.size // dim, c.size // (dim + 1)
-    w = coeffs_for(op, v, c, dim)
-    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
-    dw = torch.from_numpy(w).cuda() if w is not None else None
-    var = fb.make_variant(op, dim, prec, "strict", element_batch_size=32)
-    store = fb.integrate_mesh(var, dv, dc, dw)
-    g = fb.pack_geometry(dv, dc, dim, 32, prec)
-    plan = fb.AssemblyPlan(op, dim, dc, nv)
-    base = plan.assemble(var, store, symmetric=True)
-    sid = torch.cuda.current_stream().cuda_stream
-    for verts in (v, dv):  # host and device coordinates
-        plan.order_groups(verts)
-        assert torch.equal(plan.assemble(var, store, symmetric=True), base)
-        assert torch.equal(plan.assemble(var, store), base)
-        got = torch.full_like(base, float("nan"))
-        plan.assemble_packed_async(var, g, got, dw, sid)
-        torch.cuda.synchronize()
-        assert torch.equal(got, base)
-    plan.order_groups(None)
-    assert torch.equal(plan.assemble(var, store, symmetric=True), base)
-    with pytest.raises(_lib.InvalidArgument, match="vertex count"):
-        plan.order_groups(v[:-dim])
-    del ne

@@ -32,7 +32,6 @@ def main():
     p.add_argument("--workloads", default="3d-laplacian-16m,2d-elasticity-1m,3d-elasticity-8m")
     p.add_argument("--precisions", default="f32,f64")
     p.add_argument("--steps", type=int, default=10)
-    p.add_argument("--order", action="store_true", help="Morton group schedule (AssemblyPlan.order_groups)")
     a = p.parse_args()
     peak, peak_src = bench.peaks()
     scrub = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -54,8 +53,6 @@ def main():
         t0 = time.perf_counter()
         plan = fb.AssemblyPlan(op, dim, dc, nv)  # built on the GPU
         t_plan = time.perf_counter() - t0
-        if a.order:
-            plan.order_groups(v)
         nb = dim + 1
         kr = fb.engine.make_form_spec(op, dim).krows
         for prec in a.precisions.split(","):
