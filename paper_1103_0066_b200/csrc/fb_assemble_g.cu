@@ -12,7 +12,10 @@
 //
 // Bytes per element: G (dim^2 scalars) read once per incidence instead of an
 // element-matrix row, and no store written -- the win grows with krows^2
-// (3D elasticity: 36 B of G vs a 576 B matrix).
+// (3D elasticity: 36 B of G vs a 576 B matrix).  In 3D an incidence with
+// local index a != 0 reads only row a-1 of G and contracts the one row it
+// needs (contract_row); the CSR row block leaves with 32-byte full-sector
+// stores (fb_asm_store.cuh).
 #include <atomic>
 #include <cstdint>
 
