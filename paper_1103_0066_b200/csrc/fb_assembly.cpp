@@ -12,6 +12,7 @@
 //      row block's columns);
 //   3. per incidence, the neighbour slot of each of the element's vertices.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -27,6 +28,10 @@
 using namespace fbc;
 
 namespace {
+
+// host connectivity from this size on is planned on the GPU (FB_PLAN_HOST in
+// the environment forces the host builder)
+constexpr int64_t kGpuPlanMinElements = 1 << 16;
 
 struct DevPlan {
   int64_t* goff = nullptr;
@@ -415,6 +420,28 @@ fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t n
                            const int cdev = ne > 0 ? pointer_device(cells) : -1;
                            if (cdev >= 0)
                              build_plan_gpu(*A, cells, cdev);  // device-resident connectivity
+                           else if (ne >= kGpuPlanMinElements && device_count() > 0 && !std::getenv("FB_PLAN_HOST"))
+                           {
+                             // host connectivity of a large mesh: upload it and
+                             // build on the current GPU (same plan array for
+                             // array; 16.8 M tets: ~25 ms vs ~1 s on the host)
+                             int dev = 0;
+                             cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+                             const size_t bytes = static_cast<size_t>(ne) * (dim + 1) * sizeof(int32_t);
+                             int32_t* d = nullptr;
+                             cuda_check(cudaMalloc(&d, bytes), "cudaMalloc");
+                             try
+                             {
+                               cuda_check(cudaMemcpy(d, cells, bytes, cudaMemcpyHostToDevice), "upload cells");
+                               build_plan_gpu(*A, d, dev);
+                             }
+                             catch (...)
+                             {
+                               cudaFree(d);
+                               throw;
+                             }
+                             cudaFree(d);
+                           }
                            else
                              build_plan(*A, cells);
                          });

@@ -315,3 +315,29 @@ def test_assembly_of_an_empty_mesh(op, dim):
                                    torch.empty(0, dtype=torch.float64, device="cuda") if coeffs is not None else None,
                                    torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("op,dim", [("elasticity", 3), ("laplacian", 2)])
+def test_large_host_connectivity_is_planned_on_the_gpu(op, dim, monkeypatch):
+    import torch
+
+    # >= 65,536 elements of host connectivity: uploaded and planned on the
+    # GPU; the plan equals the host builder's (FB_PLAN_HOST) array for array
+    v, c, _ = fb.mesh_prefix(dim, 70000, 0.1)
+    cs = c.reshape(-1, dim + 1)[np.random.default_rng(2).permutation(70000)].ravel().copy()
+    nv = v.size // dim
+    for cells in (c, cs):
+        auto = fb.AssemblyPlan(op, dim, cells, nv)
+        monkeypatch.setenv("FB_PLAN_HOST", "1")
+        host = fb.AssemblyPlan(op, dim, cells, nv)
+        monkeypatch.delenv("FB_PLAN_HOST")
+        assert auto.nnz == host.nnz
+        for x, y in zip(auto.pattern(), host.pattern()):
+            assert np.array_equal(x, y)
+        var = fb.make_variant(op, dim, "f32", "strict")
+        store = fb.integrate_mesh(var, torch.from_numpy(v).cuda(), torch.from_numpy(cells).cuda())
+        assert torch.equal(auto.assemble(var, store, symmetric=True), host.assemble(var, store, symmetric=True))
+    bad = c.copy()
+    bad[(dim + 1) * 60001 + 1] = nv + 3
+    with pytest.raises(_lib.InvalidArgument, match="out of range in cell 60001"):
+        fb.AssemblyPlan(op, dim, bad, nv)

@@ -44,9 +44,16 @@ def main():
         op, dim, ne, _ = bench.WORKLOADS[w]
         v, c, _ = bench.build_rank_mesh(op, dim, ne, 0, 1)
         nv = v.size // dim
+        os.environ["FB_PLAN_HOST"] = "1"  # the multithreaded host builder
         t0 = time.perf_counter()
         fb.AssemblyPlan(op, dim, c, nv)
         t_plan_host = time.perf_counter() - t0
+        del os.environ["FB_PLAN_HOST"]
+        fb.AssemblyPlan(op, dim, c, nv)  # warm-up of the upload + GPU build path
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fb.AssemblyPlan(op, dim, c, nv)  # host cells: uploaded, planned on the GPU
+        t_plan_hostcells = time.perf_counter() - t0
         dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
         fb.AssemblyPlan(op, dim, dc, nv)  # warm-up (CUDA context, pools)
         torch.cuda.synchronize()
@@ -84,7 +91,8 @@ def main():
                  "frac": round(by / (t * 1e-3) * 1e-9 / peak, 3), "peak_GBs": peak, "peak_source": peak_src,
                  "Gnnz_s": round(plan.nnz / (t * 1e-3) * 1e-9, 2),
                  "Gelem_s": round(ne / (t * 1e-3) * 1e-9, 2), "plan_build_gpu_s": round(t_plan, 4),
-                 "plan_build_host_s": round(t_plan_host, 3)}
+                 "plan_build_host_s": round(t_plan_host, 3),
+                 "plan_build_from_host_cells_s": round(t_plan_hostcells, 4)}
             print(json.dumps(r), flush=True)
             res.append(r)
             # assembly straight from packed G (no element store), and the two
