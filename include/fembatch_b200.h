@@ -230,15 +230,17 @@ int fb_status_check(const int64_t* status, void* stream, fb_error* err);
  *   Values: A[r][s] = sum over elements e in ASCENDING order of the store
  *   entries mapping to (r, s), in engine precision from +0 -- bitwise the
  *   serial loop "for e: for (i, j): A[dof_i][dof_j] += Ae(i, j)".
- * The plan (pattern + vertex->element incidence lists) is built on the host
- * once per mesh; fb_assemble* run one deterministic gather kernel (no
- * atomics).  Only the real elements (0 .. num_elements-1) of the store are
+ * The plan (pattern + vertex->element incidence lists) is built once per
+ * mesh (GPU or host, see fb_assembly_create); fb_assemble* run one
+ * deterministic gather kernel (no atomics).  Only the real elements (0 .. num_elements-1) of the store are
  * read; padding slots are ignored. */
 typedef struct fb_assembly fb_assembly;
 
 /* cells: host or device pointer (num_elements*(dim+1) int32).  Device
- * connectivity builds the plan on that GPU, host connectivity on the host
- * (multithreaded); both give the same plan.  Errors: out-of-range vertex id
+ * connectivity builds the plan on that GPU; host connectivity of >= 65,536
+ * elements is uploaded and planned on the current GPU, smaller meshes (or
+ * any, with FB_PLAN_HOST set in the environment, or without a GPU) on the
+ * host (multithreaded); all give the same plan.  Errors: out-of-range vertex id
  * or a repeated vertex within a cell (FB_ERR_INVALID_ARGUMENT, err->cell =
  * the lowest such cell), vertex degree > 255. */
 fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t num_elements,
