@@ -232,8 +232,8 @@ int fb_status_check(const int64_t* status, void* stream, fb_error* err);
  *   serial loop "for e: for (i, j): A[dof_i][dof_j] += Ae(i, j)".
  * The plan (pattern + vertex->element incidence lists) is built once per
  * mesh (GPU or host, see fb_assembly_create); fb_assemble* run one
- * deterministic gather kernel (no atomics).  Only the real elements (0 .. num_elements-1) of the store are
- * read; padding slots are ignored. */
+ * deterministic gather kernel (no atomics).  Only the real elements
+ * (0 .. num_elements-1) of the store are read; padding slots are ignored. */
 typedef struct fb_assembly fb_assembly;
 
 /* cells: host or device pointer (num_elements*(dim+1) int32).  Device
