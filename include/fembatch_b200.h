@@ -125,6 +125,23 @@ int fb_abi_version(void);
 int fb_device_count(void);
 /* Number of CUDA kernels this library has launched so far (all devices). */
 int64_t fb_launch_counter(void);
+/* Number of per-device kernel setups (dynamic shared-memory opt-in +
+ * occupancy query of one kernel instantiation) performed on `device` so far;
+ * every device a kernel runs on gets its own (attributes are per device
+ * context).  -1 for an id outside [0, 64). */
+int64_t fb_kernel_setups(int device);
+/* Releases the grow-only staging workspace, streams and pinned status word
+ * the library keeps for `device` (-1: every device).  Must not race with a
+ * call running on that device (it takes the device's mutex). */
+int fb_release_workspace(int device, fb_error* err);
+
+/* Element-range sharding (replaces the reference's worker split,
+ * src/engine.cpp:254-281, whose threads take contiguous batch ranges):
+ * bounds[0..parts] of the contiguous, tile-aligned slot ranges a device list
+ * of `parts` devices integrates (shard g = [bounds[g], bounds[g+1])).  The
+ * store is element-major, so the shard outputs are the matching contiguous
+ * slices of the single-device store and concatenate to it bitwise. */
+int fb_shard_bounds(int64_t num_slots, int parts, int64_t* bounds, fb_error* err);
 
 /* ---- pure host helpers -------------------------------------------------- */
 int fb_krows(int op, int dim);

@@ -17,11 +17,14 @@ from .engine import (  # noqa: F401
     integrate_mesh,
     integrate_mesh_async,
     integrate_packed_async,
+    kernel_setups,
     launch_counter,
     make_form_spec,
     make_variant,
     pack_geometry,
     pack_geometry_async,
+    release_workspace,
+    shard_bounds,
     specialize_kernel,
     status_check,
     status_reset,

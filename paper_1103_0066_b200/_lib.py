@@ -39,6 +39,9 @@ SIGNATURES = {
     "fb_abi_version": (_i32, []),
     "fb_device_count": (_i32, []),
     "fb_launch_counter": (_i64, []),
+    "fb_kernel_setups": (_i64, [_i32]),
+    "fb_release_workspace": (_i32, [_i32, _E]),
+    "fb_shard_bounds": (_i32, [_i64, _i32, _vp, _E]),
     "fb_krows": (_i32, [_i32, _i32]),
     "fb_k_len": (_i64, [_i32, _i32]),
     "fb_flop_count": (_i64, [_i32, _i32, _i64]),

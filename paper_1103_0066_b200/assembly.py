@@ -15,7 +15,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib as L
-from .engine import KernelVariant, _as, _is_torch, _numel, _op, _ptr
+from .engine import KernelVariant, _as, _chk, _is_torch, _numel, _op, _ptr
 
 FB_ASSEMBLE_SYMMETRIC = 1
 
@@ -29,7 +29,7 @@ class AssemblyPlan:
     def __init__(self, op: str, dim: int, cells, num_vertices: int):
         lib = L.load()
         self.op, self.dim = op, dim
-        cells = _as(cells, np.int32)
+        cells = _as(cells, np.int32, "cells")
         self.num_elements = _numel(cells) // (dim + 1)
         self.num_vertices = int(num_vertices)
         err = L.fb_error()
@@ -69,7 +69,7 @@ class AssemblyPlan:
         ``symmetric=True`` promises bitwise-symmetric element matrices (the
         ``integrate_mesh`` output of a variant with ``path`` 0 or 3): rows are
         then read as contiguous columns.  The values do not depend on it."""
-        store = _as(store, variant.dtype)
+        store = _as(store, variant.dtype, "store")
         if values is None:
             if _is_torch(store) and store.is_cuda:
                 import torch
@@ -77,6 +77,7 @@ class AssemblyPlan:
                                      dtype=torch.float32 if variant.dtype == np.float32 else torch.float64)
             else:
                 values = np.empty(self.nnz, dtype=variant.dtype)
+        _chk(values, variant.dtype, "values")
         err = L.fb_error()
         rc = self._lib.fb_assemble(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
                                    _numel(values), FB_ASSEMBLE_SYMMETRIC if symmetric else 0, device,
@@ -86,6 +87,7 @@ class AssemblyPlan:
 
     def assemble_async(self, variant: KernelVariant, store, values, stream: int = 0, symmetric: bool = False):
         """Enqueue the assembly kernel on ``stream`` (device tensors only)."""
+        _chk(store, variant.dtype, "store"), _chk(values, variant.dtype, "values")
         err = L.fb_error()
         rc = self._lib.fb_assemble_async(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
                                          _numel(values), FB_ASSEMBLE_SYMMETRIC if symmetric else 0,
@@ -96,8 +98,8 @@ class AssemblyPlan:
         """CSR values straight from packed geometry ``g`` (host or device; the
         ``integrate_batches`` input): bitwise ``assemble(integrate_batches(g))``
         without ever storing the element matrices."""
-        g = _as(g, variant.dtype)
-        coeffs = _as(coeffs, np.float64)
+        g = _as(g, variant.dtype, "packed geometry")
+        coeffs = _as(coeffs, np.float64, "coefficients")
         if values is None:
             if _is_torch(g) and g.is_cuda:
                 import torch
@@ -105,6 +107,7 @@ class AssemblyPlan:
                                      dtype=torch.float32 if variant.dtype == np.float32 else torch.float64)
             else:
                 values = np.empty(self.nnz, dtype=variant.dtype)
+        _chk(values, variant.dtype, "values")
         err = L.fb_error()
         rc = self._lib.fb_assemble_packed(self._h, variant.handle, _ptr(g), _numel(g), _ptr(coeffs),
                                           _numel(coeffs) if coeffs is not None else 0, _ptr(values),
@@ -117,6 +120,8 @@ class AssemblyPlan:
         ``integrate_batches`` input, device tensor in engine precision): the
         element matrices are recomputed per incidence and never stored.
         Bitwise ``assemble(integrate_batches(g))``.  Device tensors only."""
+        _chk(g, variant.dtype, "packed geometry"), _chk(values, variant.dtype, "values")
+        _chk(coeffs, np.float64, "coefficients")
         err = L.fb_error()
         rc = self._lib.fb_assemble_packed_async(self._h, variant.handle, _ptr(g), _numel(g),
                                                 _ptr(coeffs) if coeffs is not None else None,

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "fb_asm_store.cuh"
+#include "fb_devcache.h"
 #include "fb_internal.h"
 
 namespace fbk {

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include "fb_asm_store.cuh"
+#include "fb_devcache.h"
 #include "fb_kernels.cuh"
 
 namespace fbk {

@@ -27,6 +27,7 @@
 
 #include "../../include/fembatch_b200.h"
 #include "fb_capi_util.h"
+#include "fb_devcache.h"
 #include "fb_host.h"
 #include "fb_internal.h"
 
@@ -144,6 +145,13 @@ void analyse_k(fb_variant& v)
 struct Buf {
   void* p = nullptr;
   size_t n = 0;
+  void release()
+  {
+    if (p)
+      cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
   void* get(size_t need)
   {
     if (need > n)
@@ -177,6 +185,35 @@ struct DeviceCtx {
     cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaMallocHost(&status_host, 2 * sizeof(long long)), "cudaMallocHost");
     ready = true;
+  }
+  // caller holds mu and has made the device current
+  void release()
+  {
+    if (!ready)
+      return;
+    for (auto& s : st)
+      cudaStreamDestroy(s);
+    cudaEventDestroy(ev);
+    cudaFreeHost(status_host);
+    for (Buf* b : {&vtx, &coeff_all, &status, &in[0], &in[1], &coeff[0], &coeff[1], &out[0], &out[1]})
+      b->release();
+    st[0] = st[1] = nullptr;
+    ev = nullptr;
+    status_host = nullptr;
+    ready = false;
+  }
+};
+
+// Restores the calling thread's current device on every exit path: the
+// blocking entry points switch devices internally (run_on_device) and must
+// not leave the caller on another GPU.
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() { cudaGetDevice(&dev); }
+  ~DeviceGuard()
+  {
+    if (dev >= 0)
+      cudaSetDevice(dev);
   }
 };
 
@@ -280,12 +317,41 @@ void launch_integrate_chunked(const fbk::LaunchSpec& spec, const fbk::LaunchArgs
   }
 }
 
+// pack_geometry: the same 2^30-slot split (32-bit local slot indices)
+void launch_pack_chunked(int dim, int prec, const fbk::LaunchArgs& a, cudaStream_t st)
+{
+  const int64_t dd = static_cast<int64_t>(dim) * dim;
+  for (int64_t off = 0; off < a.nloc; off += kMaxLaunchSlots)
+  {
+    fbk::LaunchArgs c = a;
+    c.slot0 = a.slot0 + off;
+    c.nloc = std::min(kMaxLaunchSlots, a.nloc - off);
+    c.out = static_cast<char*>(a.out) + off * dd * scalar_size(prec);
+    cuda_check(fbk::launch_pack(dim, prec, c, st), "pack kernel launch");
+  }
+}
+
 void launch(const Job& j, const fbk::LaunchArgs& a, cudaStream_t st)
 {
   if (j.kind == Kind::Pack)
-    cuda_check(fbk::launch_pack(j.dim, j.prec, a, st), "pack kernel launch");
+    launch_pack_chunked(j.dim, j.prec, a, st);
   else
     launch_integrate_chunked(j.spec, a, j.var->kp, j.nk, j.dim * j.dim, scalar_size(j.prec), st);
+}
+
+// Contiguous tile-aligned slot shards of a device list: outputs
+// concatenate.  Exported as fb_shard_bounds.
+std::vector<int64_t> shard_bounds(int64_t nslots, int parts)
+{
+  if (parts < 1)
+    invalid("worker count must be >= 1");
+  if (nslots < 0)
+    invalid("negative slot count");
+  const int64_t tiles = fbk::num_tiles(nslots);
+  std::vector<int64_t> bound(parts + 1);
+  for (int g = 0; g <= parts; ++g)
+    bound[g] = std::min(nslots, tiles * g / parts * fbk::kTile);
+  return bound;
 }
 
 // Runs slots [s0, s1) of the job on device `dev`.  Host buffers are staged in
@@ -420,6 +486,7 @@ void run_on_device(const Job& j, int dev, int64_t s0, int64_t s1, long long* sta
 
 void run_job(const Job& j, const int* devices, int ndev)
 {
+  DeviceGuard keep_device;  // the caller's current device survives the call
   const int have = device_count();
   if (have == 0)
     throw_code(FB_ERR_NO_DEVICE, "no CUDA device available");
@@ -449,10 +516,7 @@ void run_job(const Job& j, const int* devices, int ndev)
 
   // contiguous tile-aligned slot shards: outputs concatenate
   const int P = static_cast<int>(devs.size());
-  const int64_t tiles = fbk::num_tiles(j.nslots);
-  std::vector<int64_t> bound(P + 1);
-  for (int g = 0; g <= P; ++g)
-    bound[g] = std::min(j.nslots, tiles * g / P * fbk::kTile);
+  const std::vector<int64_t> bound = shard_bounds(j.nslots, P);
   std::vector<std::array<long long, 2>> st(P, {kStatusInit, kStatusInit});
   std::vector<std::exception_ptr> errs(P);
   auto body = [&](int g)
@@ -554,6 +618,50 @@ extern "C" {
 int fb_abi_version(void) { return FB_ABI_VERSION; }
 int fb_device_count(void) { return device_count(); }
 int64_t fb_launch_counter(void) { return fbk::launch_counter().load(); }
+
+int64_t fb_kernel_setups(int device)
+{
+  if (device < 0 || device >= fbk::kMaxDevices)
+    return -1;
+  return fbk::device_setup_counters()[device].load();
+}
+
+int fb_release_workspace(int device, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   DeviceGuard keep_device;
+                   std::vector<std::pair<int, DeviceCtx*>> todo;
+                   {
+                     std::lock_guard<std::mutex> lock(g_ctx_mu);
+                     for (auto& [d, c] : contexts())
+                       if (device < 0 || d == device)
+                         todo.emplace_back(d, c.get());
+                   }
+                   for (auto& [d, c] : todo)
+                   {
+                     std::lock_guard<std::mutex> lock(c->mu);
+                     if (!c->ready)
+                       continue;
+                     cuda_check(cudaSetDevice(d), "cudaSetDevice");
+                     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+                     c->release();
+                   }
+                 });
+}
+
+int fb_shard_bounds(int64_t num_slots, int parts, int64_t* bounds, fb_error* err)
+{
+  return guarded(err,
+                 [&]
+                 {
+                   if (!bounds)
+                     invalid("null bounds buffer");
+                   const std::vector<int64_t> b = shard_bounds(num_slots, parts);
+                   std::copy(b.begin(), b.end(), bounds);
+                 });
+}
 
 int fb_krows(int op, int dim)
 {
@@ -866,15 +974,9 @@ int fb_pack_geometry_async(const fb_mesh_view* mesh, int bs, int precision, void
                    a.ne = mesh->num_elements;
                    a.cells_aligned16 = aligned16(a.cells);
                    a.vtx_aligned16 = aligned16(a.vtx);
-                   for (int64_t off = 0; off < nslots; off += kMaxLaunchSlots)
-                   {
-                     fbk::LaunchArgs c = a;
-                     c.slot0 = off;
-                     c.nloc = std::min(kMaxLaunchSlots, nslots - off);
-                     c.out = static_cast<char*>(g_out) + off * dd * scalar_size(precision);
-                     cuda_check(fbk::launch_pack(mesh->dim, precision, c, static_cast<cudaStream_t>(stream)),
-                                "pack kernel launch");
-                   }
+                   a.slot0 = 0;
+                   a.nloc = nslots;
+                   launch_pack_chunked(mesh->dim, precision, a, static_cast<cudaStream_t>(stream));
                  });
 }
 

@@ -4,6 +4,7 @@
 
 #include <atomic>
 
+#include "fb_devcache.h"
 #include "fb_kernels.cuh"
 
 namespace fbk {
@@ -12,28 +13,32 @@ namespace fbk {
 std::atomic<long long>& launch_counter();
 
 // Persistent grid: every resident CTA slot on the device, capped by the tile
-// count (cached per kernel instantiation; all devices in a box are B200s).
+// count.  The shared-memory opt-in and the occupancy query run once per
+// kernel instantiation PER DEVICE (fb_devcache.h): attributes belong to the
+// device context, so a device list or a multi-GPU process sets up each GPU.
 template <class F>
-unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, std::atomic<int>& slots,
+unsigned persistent_grid(F kernel, int threads, int64_t nctas, size_t smem, PerDevice& slots,
                          int cap_per_sm = 1 << 20, bool persistent = true)
 {
-  int per = slots.load(std::memory_order_relaxed);
-  if (per == 0)
-  {
-    int blocks = 0, dev = 0, sms = 0;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int per = slots.get(
+      dev,
+      [&]
+      {
+        int blocks = 0, sms = 0;
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 #ifdef FB_CARVEOUT
-    // A/B: preferred shared-memory carveout (percent of the maximum); the
-    // rest of the 256 KB per SM is L1 for the coordinate gathers
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, FB_CARVEOUT);
+        // A/B: preferred shared-memory carveout (percent of the maximum); the
+        // rest of the 256 KB per SM is L1 for the coordinate gathers
+        cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, FB_CARVEOUT);
 #endif
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    blocks = blocks < cap_per_sm ? blocks : cap_per_sm;
-    per = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
-    slots.store(per, std::memory_order_relaxed);
-  }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        blocks = blocks < cap_per_sm ? blocks : cap_per_sm;
+        return (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
+      },
+      device_setup_counters());
 #ifdef FB_NONPERSIST  // A/B: one warp tile per warp everywhere
   persistent = false;
 #endif
@@ -62,7 +67,7 @@ cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st
   }
   auto kernel = fb_integrate_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, ST>;
   constexpr size_t smem = sparse_smem_bytes<S, DIM, OP, SYM, ST>();
-  static std::atomic<int> slots{0};  // one cache per kernel instantiation
+  static PerDevice slots;  // one cache per kernel instantiation and device
   constexpr int threads = kWarpsPerCta * 32;
   const int64_t nctas = (a.nloc + threads - 1) / threads;
   kernel<<<persistent_grid(kernel, threads, nctas, smem, slots, sparse_cta_cap<DIM, OP>(),

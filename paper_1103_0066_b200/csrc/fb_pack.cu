@@ -9,6 +9,12 @@ std::atomic<long long>& launch_counter()
   return counter;
 }
 
+std::atomic<long long>* device_setup_counters()
+{
+  static std::atomic<long long> counters[kMaxDevices] = {};
+  return counters;
+}
+
 // GPU pack_geometry (src/geometry.cpp:312-351) = the sparse kernel's
 // warp-tile pipeline with G itself as the per-slot output (OP = kPack):
 // prefetched gathers, FP64 geometry with the reference's exact zero signs,

@@ -175,9 +175,29 @@ def _numel(x) -> int:
     return x.numel() if _is_torch(x) else x.size
 
 
-def _as(x, dtype):
-    if x is None or _is_torch(x):
+def _dtype_name(x) -> str:
+    return str(x.dtype).replace("torch.", "")
+
+
+def _chk(x, dtype, name: str = "array"):
+    """Checks (never casts) the element type of an array the C ABI reads or
+    writes as raw `dtype` scalars: a torch int64 cells tensor or an f32 store
+    passed where f64 is expected would otherwise be reinterpreted."""
+    if x is None:
         return x
+    want = np.dtype(dtype)
+    if _dtype_name(x) != want.name:
+        raise L.InvalidArgument(1, f"{name} has dtype {_dtype_name(x)}; {want.name} is required")
+    return x
+
+
+def _as(x, dtype, name: str = "array"):
+    """Host arrays are converted to `dtype` (a copy when needed); torch tensors
+    are passed through without a copy and must already have it."""
+    if x is None:
+        return x
+    if _is_torch(x):
+        return _chk(x, dtype, name)
     return np.ascontiguousarray(x, dtype=dtype)
 
 
@@ -211,12 +231,13 @@ def integrate_mesh(variant: KernelVariant, vertices, cells, coefficients=None, o
     """
     lib = L.load()
     dim = variant.spec.dim
-    vertices, cells = _as(vertices, np.float64), _as(cells, np.int32)
-    coefficients = _as(coefficients, np.float64)
+    vertices, cells = _as(vertices, np.float64, "vertices"), _as(cells, np.int32, "cells")
+    coefficients = _as(coefficients, np.float64, "coefficients")
     ne = _numel(cells) // (dim + 1)
     n = variant.store_length(ne)
     if out is None:
         out = _alloc_out(variant, n, cells)
+    _chk(out, variant.dtype, "out")
     mv = mesh_view(vertices, cells, dim)
     dv, nd = _devs(devices)
     err = L.fb_error()
@@ -231,8 +252,8 @@ def integrate_batches(variant: KernelVariant, g, num_elements: int, coefficients
     """Reference integrate_batches on packed G (slot-major, engine precision)."""
     lib = L.load()
     dim = variant.spec.dim
-    g = _as(g, variant.dtype)
-    coefficients = _as(coefficients, np.float64)
+    g = _as(g, variant.dtype, "packed geometry")
+    coefficients = _as(coefficients, np.float64, "coefficients")
     bs = variant.config.element_batch_size
     nslots = _numel(g) // (dim * dim)
     if nslots % bs:
@@ -240,6 +261,7 @@ def integrate_batches(variant: KernelVariant, g, num_elements: int, coefficients
     n = nslots * variant.spec.krows ** 2
     if out is None:
         out = _alloc_out(variant, n, g)
+    _chk(out, variant.dtype, "out")
     dv, nd = _devs(devices)
     err = L.fb_error()
     rc = lib.fb_integrate_packed(variant.handle, dim, _ptr(g), nslots // bs, num_elements,
@@ -252,7 +274,7 @@ def pack_geometry(vertices, cells, dim: int, element_batch_size: int = 128,
                   precision: str = "f64", out=None, devices: Optional[Sequence[int]] = None):
     """GPU pack_geometry: G in the reference PackedGeometry layout."""
     lib = L.load()
-    vertices, cells = _as(vertices, np.float64), _as(cells, np.int32)
+    vertices, cells = _as(vertices, np.float64, "vertices"), _as(cells, np.int32, "cells")
     ne = _numel(cells) // (dim + 1)
     n = -(-ne // element_batch_size) * element_batch_size * dim * dim
     if out is None:
@@ -262,6 +284,7 @@ def pack_geometry(vertices, cells, dim: int, element_batch_size: int = 128,
                               device=cells.device)
         else:
             out = np.empty(n, dtype=scalar_dtype(precision))
+    _chk(out, scalar_dtype(precision), "out")
     mv = mesh_view(vertices, cells, dim)
     dv, nd = _devs(devices)
     err = L.fb_error()
@@ -275,6 +298,9 @@ def integrate_mesh_async(variant: KernelVariant, vertices, cells, out, status, s
                          coefficients=None):
     """Enqueue the fused kernel on ``stream`` (device tensors only; no sync)."""
     lib = L.load()
+    _chk(vertices, np.float64, "vertices"), _chk(cells, np.int32, "cells")
+    _chk(coefficients, np.float64, "coefficients"), _chk(out, variant.dtype, "out")
+    _chk(status, np.int64, "status")
     mv = mesh_view(vertices, cells, variant.spec.dim)
     err = L.fb_error()
     rc = lib.fb_integrate_mesh_async(variant.handle, C.byref(mv), _ptr(coefficients), _ptr(out),
@@ -286,6 +312,8 @@ def integrate_packed_async(variant: KernelVariant, g, num_elements: int, out, st
                            coefficients=None):
     lib = L.load()
     dim = variant.spec.dim
+    _chk(g, variant.dtype, "packed geometry"), _chk(out, variant.dtype, "out")
+    _chk(coefficients, np.float64, "coefficients")
     nslots = _numel(g) // (dim * dim)
     err = L.fb_error()
     rc = lib.fb_integrate_packed_async(variant.handle, dim, _ptr(g),
@@ -298,6 +326,8 @@ def integrate_packed_async(variant: KernelVariant, g, num_elements: int, out, st
 def pack_geometry_async(vertices, cells, dim: int, g_out, status, element_batch_size: int = 128,
                         precision: str = "f64", stream: int = 0):
     """Enqueue the GPU pack_geometry kernel on ``stream`` (device tensors only)."""
+    _chk(vertices, np.float64, "vertices"), _chk(cells, np.int32, "cells")
+    _chk(g_out, scalar_dtype(precision), "g_out"), _chk(status, np.int64, "status")
     mv = mesh_view(vertices, cells, dim)
     err = L.fb_error()
     rc = L.load().fb_pack_geometry_async(C.byref(mv), element_batch_size, _prec(precision), _ptr(g_out),
@@ -306,11 +336,13 @@ def pack_geometry_async(vertices, cells, dim: int, g_out, status, element_batch_
 
 
 def status_reset(status, stream: int = 0):
+    _chk(status, np.int64, "status")
     err = L.fb_error()
     L.raise_for(L.load().fb_status_reset(_ptr(status), C.c_void_p(stream), C.byref(err)), err)
 
 
 def status_check(status, stream: int = 0):
+    _chk(status, np.int64, "status")
     err = L.fb_error()
     L.raise_for(L.load().fb_status_check(_ptr(status), C.c_void_p(stream), C.byref(err)), err)
 
@@ -341,3 +373,24 @@ def launch_counter() -> int:
 
 def device_count() -> int:
     return L.load().fb_device_count()
+
+
+def kernel_setups(device: int) -> int:
+    """Per-device kernel setups (shared-memory opt-in + occupancy) so far."""
+    return L.load().fb_kernel_setups(device)
+
+
+def release_workspace(device: int = -1) -> None:
+    """Free the library's staging workspace and streams on ``device`` (-1: all)."""
+    err = L.fb_error()
+    L.raise_for(L.load().fb_release_workspace(device, C.byref(err)), err)
+
+
+def shard_bounds(num_slots: int, parts: int) -> list:
+    """The engine's element-range split for a device list (fb_shard_bounds):
+    ``[b_0 = 0, ..., b_parts = num_slots]``, contiguous and tile aligned; shard g
+    integrates slots ``[b_g, b_g+1)`` and its output is that slice of the store."""
+    b = (C.c_int64 * (max(parts, 0) + 1))()
+    err = L.fb_error()
+    L.raise_for(L.load().fb_shard_bounds(num_slots, parts, b, C.byref(err)), err)
+    return list(b)

@@ -148,3 +148,15 @@ def test_device_alloc_without_a_gpu_fails_loudly():
         assert lib.fb_device_alloc(1024, 0, ctypes.byref(err)) is None
         assert err.code == _lib.FB_ERR_NO_DEVICE
     assert lib.fb_free(None, ctypes.byref(err)) == _lib.FB_OK
+
+
+def test_host_dtype_checks_without_gpu(fb):
+    """Output buffers are never reinterpreted: a wrong-precision numpy `out`
+    is rejected before any device work (no GPU needed to reach the check)."""
+    import numpy as np
+    import pytest
+
+    v, c = fb.structured_mesh(2, 4, 0.0, 42)
+    var = fb.make_variant("laplacian", 2, "f32")
+    with pytest.raises(fb.engine.L.InvalidArgument, match="out has dtype float64"):
+        fb.integrate_mesh(var, v, c, out=np.empty(var.store_length(c.size // 3)))

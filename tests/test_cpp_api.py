@@ -48,3 +48,11 @@ def test_c_abi_from_plain_c_host():
 def test_c_abi_from_plain_c_gpu():
     r = subprocess.run([_binary(CBIN), "all"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_per_device_kernel_setup_cache():
+    """fb_devcache.h: launch setup runs once for every device id, not once per process."""
+    r = subprocess.run([_binary(os.path.join(HERE, "cpp", "_bin", "test_devcache"))], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout

@@ -44,6 +44,12 @@ for op, dim, n, prec in (("elasticity", 2, 20, "f32"), ("laplacian", 3, 8, "f64"
     fb.integrate_packed_async(var, g, ne, out2, sid, coefficients=dw)
     torch.cuda.synchronize()
     assert out2.cpu().numpy().tobytes() == want.tobytes(), ("packed", op, dim, prec)
+    # the blocking pack_geometry splits its device-resident launch the same way
+    k0 = fb.launch_counter()
+    g2 = fb.pack_geometry(dv, dc, dim, 128, prec)
+    torch.cuda.synchronize()
+    assert fb.launch_counter() - k0 > 1, "blocking pack_geometry was not split"
+    assert g2.cpu().numpy().tobytes() == g.cpu().numpy().tobytes()
 print("launches", fb.launch_counter() - n0)
 '''
 

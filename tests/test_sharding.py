@@ -1,9 +1,10 @@
-"""Multi-rank sharding on CPU (gloo, world_size 2): contiguous tile-aligned
-shards integrate independently and concatenate to the single-device store
-bitwise -- the property that lets the GPU path shard over 8 B200s with no
-collective.  Shards are integrated with the oracle
-restatement here (no GPU); tests/test_gpu_parity.py checks the CUDA path's
-own multi-device split (devices=[0, 0, 0]) against the single launch."""
+"""Multi-rank sharding (gloo, world_size 2): the engine's own element-range
+split (fb_shard_bounds, the function run_job uses for a device list) gives
+contiguous tile-aligned shards that integrate independently and concatenate
+to the single-device store bitwise -- the property that lets the GPU path
+shard over 8 B200s with no collective.  On CPU the
+shards are integrated with the oracle restatement; the gpu-marked variant
+integrates each rank's shard with the CUDA engine (both ranks on cuda:0)."""
 import os
 import socket
 
@@ -13,17 +14,28 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1103_0066_b200.shard import TILE, rank_elements, shard_bounds
+import paper_1103_0066_b200 as fb
+
+TILE = 288  # fbk::kTile (csrc/fb_internal.h)
 
 
 def test_shard_bounds_cover_and_align():
-    for nslots in (0, 1, 287, 288, 289, 10_000, 1 << 20):
+    for nslots in (0, 1, 287, 288, 289, 10_000, 1 << 20, 1 << 34):
         for parts in (1, 2, 3, 8):
-            b = shard_bounds(nslots, parts)
+            b = fb.shard_bounds(nslots, parts)
             assert b[0] == 0 and b[-1] == nslots and len(b) == parts + 1
             assert all(x <= y for x, y in zip(b, b[1:]))
             assert all(x % TILE == 0 for x in b[:-1])
-    assert rank_elements(1 << 20, 3) == (3 << 20, 4 << 20)
+            if nslots >= TILE * parts:  # balanced to within one tile
+                sizes = [y - x for x, y in zip(b, b[1:])]
+                assert max(sizes) - min(sizes) <= TILE
+
+
+def test_shard_bounds_rejects_bad_counts():
+    with pytest.raises(fb.engine.L.InvalidArgument, match="worker count"):
+        fb.shard_bounds(100, 0)
+    with pytest.raises(fb.engine.L.InvalidArgument):
+        fb.shard_bounds(-1, 2)
 
 
 def _free_port():
@@ -34,7 +46,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, op, dim, bs, prec, q):
+def _worker(rank, world, port, op, dim, bs, prec, q, on_gpu=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -50,12 +62,17 @@ def _worker(rank, world, port, op, dim, bs, prec, q):
         nslots = -(-ne // bs) * bs
         full = ora.integrate_mesh(op, v, c, dim, bs=bs, precision=prec)
         nk = full.size // nslots
-        b = shard_bounds(nslots, world)
+        b = fb.shard_bounds(nslots, world)
         s0, s1 = b[rank], b[rank + 1]
         # the shard: slots [s0, s1); padding slots replicate element ne-1
         ids = np.minimum(np.arange(s0, s1), ne - 1)
         cs = np.ascontiguousarray(c.reshape(-1, nb)[ids].ravel())
-        part = ora.integrate_mesh(op, v, cs, dim, bs=1, precision=prec)
+        if on_gpu:
+            var = fb.make_variant(op, dim, "f32" if prec == 0 else "f64", "strict", element_batch_size=1)
+            part = fb.integrate_mesh(var, torch.from_numpy(v).cuda(), torch.from_numpy(cs).cuda()).cpu().numpy()
+            assert fb.kernel_setups(0) > 0  # the kernel was set up on this rank's device
+        else:
+            part = ora.integrate_mesh(op, v, cs, dim, bs=1, precision=prec)
         sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(sizes, torch.tensor([part.size]))
         n = int(max(x.item() for x in sizes))
@@ -71,15 +88,26 @@ def _worker(rank, world, port, op, dim, bs, prec, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("op,dim,bs,prec", [("elasticity", 2, 128, 0), ("laplacian", 3, 7, 1)])
-def test_gloo_two_rank_shards_concatenate_bitwise(op, dim, bs, prec):
+def _run_two_ranks(op, dim, bs, prec, on_gpu):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, op, dim, bs, prec, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, op, dim, bs, prec, q, on_gpu)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=300)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) is True
+
+
+@pytest.mark.parametrize("op,dim,bs,prec", [("elasticity", 2, 128, 0), ("laplacian", 3, 7, 1)])
+def test_gloo_two_rank_shards_concatenate_bitwise(op, dim, bs, prec):
+    _run_two_ranks(op, dim, bs, prec, on_gpu=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("op,dim,bs,prec", [("elasticity", 3, 128, 0), ("laplacian", 2, 5, 1)])
+def test_gloo_two_rank_engine_shards_concatenate_bitwise(op, dim, bs, prec):
+    """Each rank integrates its engine-split shard with the CUDA engine."""
+    _run_two_ranks(op, dim, bs, prec, on_gpu=True)
