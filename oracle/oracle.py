@@ -359,6 +359,38 @@ class Reference:
         return mn.value, mean.value
 
 
+def structured_mesh_numpy(dim: int, n: int):
+    """Unjittered structured_simplicial_mesh (reference geometry.cpp:164-234)
+    in numpy: vertex (i, j[, k]) / n in lexicographic order; two triangles per
+    square / six tetrahedra per cube along the vertex paths (0,..,0) ->
+    (1,..,1), odd permutations with vertices 1 and 2 swapped."""
+    m = n + 1
+    g = np.arange(m, dtype=np.float64) / n
+    if dim == 2:
+        jj, ii = np.meshgrid(g, g, indexing="ij")
+        v = np.stack([ii.ravel(), jj.ravel()], axis=1).ravel()
+        j, i = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        v00 = (i + j * m).ravel()
+        v10, v01, v11 = v00 + 1, v00 + m, v00 + m + 1
+        c = np.stack([v00, v10, v11, v00, v11, v01], axis=1).reshape(-1, 3)
+        return v, np.ascontiguousarray(c.astype(np.int32).ravel())
+    kk, jj, ii = np.meshgrid(g, g, g, indexing="ij")
+    v = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).ravel()
+    k, j, i = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    base = (i + m * (j + m * k)).ravel().astype(np.int64)
+    unit = [1, m, m * m]
+    perms = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+    odd = [False, True, True, False, False, True]
+    tets = []
+    for p, o in zip(perms, odd):
+        a = base + unit[p[0]]
+        b = a + unit[p[1]]
+        d = b + unit[p[2]]
+        tets.append(np.stack([base, b, a, d] if o else [base, a, b, d], axis=1))
+    c = np.stack(tets, axis=1).reshape(-1, 4)
+    return v, np.ascontiguousarray(c.astype(np.int32).ravel())
+
+
 def reference_available() -> bool:
     return os.path.exists(LIB_REFERENCE)
 

@@ -1,6 +1,8 @@
 """Write profiles/ncu_traffic.json: per-launch DRAM traffic of the top kernel
 (dram__bytes_read.sum + dram__bytes_write.sum from one `ncu --set full`
 capture) keyed "workload:precision:mode", read by bench.py's roofline block.
+Each entry records the hash of the kernel sources it was captured on
+(bench.kernel_source_sha); bench.py reports traffic null once they change.
 
     python tools/ncu_traffic.py KEY report.ncu-rep [KEY report ...]
 """
@@ -30,8 +32,12 @@ def traffic(rep):
 def main():
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
     args = sys.argv[1:]
+    sys.path.insert(0, ROOT)
+    import bench
+
+    sha = bench.kernel_source_sha()
     for key, rep in zip(args[::2], args[1::2]):
-        data[key] = traffic(rep)
+        data[key] = {"traffic": traffic(rep), "kernel_sha": sha, "report": os.path.basename(rep)}
         print(key, data[key])
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as f:
