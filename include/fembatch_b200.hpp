@@ -258,44 +258,12 @@ CsrMatrix assemble_global(const KernelVariant& variant, const AssemblyPlan& plan
 CsrMatrix assemble_global(const KernelVariant& variant, const AssemblyPlan& plan, const PackedGeometry& geometry,
                           const std::vector<double>& coefficients = {}, int device = 0);
 
-// ---- verification (reference include/fembatch/oracle.hpp) ----------------
-// An independent FP64 element matrix by direct quadrature in physical space
-// (pulled-back P1 gradients per quadrature point; never G or K) and a store
-// checker built on it, for callers that want to check results.  Host code;
-// the integration and assembly paths never call it.
-struct OracleReport {
-  double max_rel_error = 0.0;  // |got - exact| / max(|exact|, 1e-14)
-  double max_abs_error = 0.0;
-  std::int64_t worst_element = -1;
-  int worst_test_index = -1;
-  int worst_trial_index = -1;
-  double tolerance = 0.0;
-  bool passed = false;
-};
-// Row-major krows x krows; vertex_coords (dim+1)*dim; coefficients: nb nodal
-// values for the weighted form, empty otherwise (std::invalid_argument).
-std::vector<double> assemble_element_direct(const FormSpec& spec, std::span<const double> vertex_coords,
-                                            std::span<const double> coefficients = {});
-OracleReport verify(const ElementMatrixStore& store, const Mesh& mesh, const FormSpec& spec,
-                    const KernelConfig& config, const CoefficientField* coefficients, double tolerance);
-
 // ---- benchmark records (reference include/fembatch/bench.hpp) ------------
-// run_benchmark times this engine's API calls (integrate_batches on the GPU,
-// plus pack_geometry with include_packing) by wall clock, host data in and
-// out, like the reference times its CPU engine; records and their CSV/JSON
-// forms are the reference's, field for field.
-struct BenchOptions {
-  Operator op = Operator::laplacian;
-  int dim = 3;
-  int n = 16;  // structured mesh resolution
-  double jitter = 0.0;
-  std::uint64_t seed = 42;
-  KernelConfig config;
-  int workers = 1;
-  int repetitions = 3;
-  bool include_packing = false;
-  bool verify_first = false;
-};
+// The record and its CSV / JSON forms, field for field
+// the reference's, and the store checksum (row A16).  The benchmark RUNNER
+// (run_benchmark, sweep) and the verification module are reference tooling
+// outside the hot path: they live in the separate compatibility library
+// (include/fembatch_compat.hpp, compat/libfembatch_compat.so).
 struct BenchRecord {
   std::string op;
   int dim = 0;
@@ -314,20 +282,9 @@ struct BenchRecord {
   std::string status;
   friend bool operator==(const BenchRecord&, const BenchRecord&) = default;
 };
-// Axis values sorted and deduplicated; rows in lexicographic (bs, ce,
-// interleave, unroll) order; invalid points become status rows.
-struct SweepGrid {
-  BenchOptions base;
-  std::vector<int> batch_sizes{16, 32, 64, 128};
-  std::vector<int> concurrent{1, 2, 4};
-  std::vector<bool> interleave{false, true};
-  std::vector<bool> unroll{false, true};
-};
 CoefficientField default_coefficient_field(const Mesh& mesh);  // w = 1 + x0 at cell vertices
 double store_checksum(const ElementMatrixStore& store);        // real entries, element order, in double
 double default_tolerance(Precision p);                         // 1e-12 f64, 5e-5 f32
-BenchRecord run_benchmark(const BenchOptions& options);
-std::vector<BenchRecord> sweep(const SweepGrid& grid);
 extern const char* const csv_header;
 void write_csv(std::ostream& os, const std::vector<BenchRecord>& records);
 std::vector<BenchRecord> read_csv(std::istream& is);

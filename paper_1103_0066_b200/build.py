@@ -33,10 +33,10 @@ CU_SOURCES = [
     "fb_plan.cu",
     "fb_assemble_g.cu",
 ]
-CPP_SOURCES = ["fb_capi.cpp", "fb_assembly.cpp", "fb_host.cpp", "fembatch_api.cpp", "fembatch_verify.cpp",
-               "fembatch_bench.cpp"]
+CPP_SOURCES = ["fb_capi.cpp", "fb_assembly.cpp", "fb_host.cpp", "fembatch_api.cpp", "fembatch_records.cpp"]
 CU_HOST_SOURCES = ["fb_tma.cpp"]  # host code that includes the kernel headers (nvcc)
-HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h", "fb_capi_util.h", "fb_asm_store.cuh"]
+HEADERS = ["fb_internal.h", "fb_kernels.cuh", "fb_launch.cuh", "fb_host.h", "fb_capi_util.h", "fb_asm_store.cuh",
+           "fb_devcache.h"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "fembatch_b200.h"),
                   os.path.join(ROOT, "include", "fembatch_b200.hpp")]
 
