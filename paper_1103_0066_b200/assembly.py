@@ -4,9 +4,13 @@ The reference stops at element matrices (global assembly is its declared
 non-goal, ``SPEC.md:370``); this is the consumer a finite-element code puts
 after ``integrate_mesh``.  ``AssemblyPlan`` wraps the C ABI's
 ``fb_assembly`` (``include/fembatch_b200.h``, "global assembly"): the CSR
-pattern and vertex->element incidence lists are built once per mesh on the
-host, and ``assemble`` runs one deterministic gather kernel on the GPU whose
-result is bitwise the serial element-order sum.
+pattern and vertex->element incidence lists are built once per mesh -- on
+the GPU for device-resident connectivity and for host meshes of 65,536 or
+more elements (uploaded; a CUDA failure there falls back to the host
+builder), on the host otherwise or with ``FB_PLAN_HOST=1`` (both builders
+give the same plan and the same error for the same bad cell) -- and
+``assemble`` runs one deterministic gather kernel on the GPU whose result is
+bitwise the serial element-order sum.
 """
 from __future__ import annotations
 

@@ -237,10 +237,21 @@ void build_plan_gpu(fb_assembly& A, const int32_t* cells, int dev)
   p.nbr = P.nbr;
   if (bad[0] >= 0 || bad[1] >= 0)
   {
-    const bool range = bad[0] >= 0 && (bad[1] < 0 || bad[0] < bad[1]);
-    const int64_t c = range ? bad[0] : bad[1];
-    throw_code(FB_ERR_INVALID_ARGUMENT,
-               (range ? "cell vertex index out of range in cell " : "repeated vertex in cell ") + std::to_string(c), c);
+    // the lowest offending cell, and its failure reported exactly as the
+    // host builder would (first bad slot in slot order): its ids are
+    // rechecked on the host
+    const int64_t c = bad[0] < 0 ? bad[1] : (bad[1] < 0 ? bad[0] : std::min(bad[0], bad[1]));
+    int32_t ids[4] = {0, 0, 0, 0};
+    cuda_check(cudaMemcpy(ids, cells + c * A.nb, A.nb * sizeof(int32_t), cudaMemcpyDefault), "download cell");
+    for (int a = 0; a < A.nb; ++a)
+    {
+      if (ids[a] < 0 || ids[a] >= A.nv)
+        throw_code(FB_ERR_INVALID_ARGUMENT, "cell vertex index out of range in cell " + std::to_string(c), c);
+      for (int b = 0; b < a; ++b)
+        if (ids[b] == ids[a])
+          throw_code(FB_ERR_INVALID_ARGUMENT, "repeated vertex in cell " + std::to_string(c), c);
+    }
+    throw_code(FB_ERR_INVALID_ARGUMENT, "cell vertex index out of range in cell " + std::to_string(c), c);
   }
   A.home = dev;
   A.dev.emplace(dev, p);  // owned from here on (freed by ~fb_assembly)
@@ -410,13 +421,17 @@ fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t n
                              invalid("mesh sizes out of range for assembly");
                            if (ne > 0 && !cells)
                              invalid("null cells");
-                           A = std::make_unique<fb_assembly>();
-                           A->op = op;
-                           A->dim = dim;
-                           A->nb = dim + 1;
-                           A->nc = op == FB_ELASTICITY ? dim : 1;
-                           A->nv = nv;
-                           A->ne = ne;
+                           auto fresh = [&]
+                           {
+                             A = std::make_unique<fb_assembly>();
+                             A->op = op;
+                             A->dim = dim;
+                             A->nb = dim + 1;
+                             A->nc = op == FB_ELASTICITY ? dim : 1;
+                             A->nv = nv;
+                             A->ne = ne;
+                           };
+                           fresh();
                            const int cdev = ne > 0 ? pointer_device(cells) : -1;
                            if (cdev >= 0)
                              build_plan_gpu(*A, cells, cdev);  // device-resident connectivity
@@ -424,23 +439,42 @@ fb_assembly* fb_assembly_create(int op, int dim, const int32_t* cells, int64_t n
                            {
                              // host connectivity of a large mesh: upload it and
                              // build on the current GPU (same plan array for
-                             // array; 16.8 M tets: ~25 ms vs ~1 s on the host)
-                             int dev = 0;
-                             cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-                             const size_t bytes = static_cast<size_t>(ne) * (dim + 1) * sizeof(int32_t);
-                             int32_t* d = nullptr;
-                             cuda_check(cudaMalloc(&d, bytes), "cudaMalloc");
+                             // array; 16.8 M tets: ~25 ms vs ~1 s on the host).
+                             // A CUDA failure there (out of memory, a device
+                             // in exclusive use) falls back to the host builder;
+                             // invalid input still fails as invalid input.
+                             bool gpu_ok = false;
                              try
                              {
-                               cuda_check(cudaMemcpy(d, cells, bytes, cudaMemcpyHostToDevice), "upload cells");
-                               build_plan_gpu(*A, d, dev);
-                             }
-                             catch (...)
-                             {
+                               int dev = 0;
+                               cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+                               const size_t bytes = static_cast<size_t>(ne) * (dim + 1) * sizeof(int32_t);
+                               int32_t* d = nullptr;
+                               cuda_check(cudaMalloc(&d, bytes), "cudaMalloc");
+                               try
+                               {
+                                 cuda_check(cudaMemcpy(d, cells, bytes, cudaMemcpyHostToDevice), "upload cells");
+                                 build_plan_gpu(*A, d, dev);
+                               }
+                               catch (...)
+                               {
+                                 cudaFree(d);
+                                 throw;
+                               }
                                cudaFree(d);
-                               throw;
+                               gpu_ok = true;
                              }
-                             cudaFree(d);
+                             catch (const Error& e)
+                             {
+                               if (e.code != FB_ERR_CUDA)
+                                 throw;
+                               cudaGetLastError();  // clear the sticky-free error state
+                             }
+                             if (!gpu_ok)
+                             {
+                               fresh();
+                               build_plan(*A, cells);
+                             }
                            }
                            else
                              build_plan(*A, cells);

@@ -220,9 +220,33 @@ template <int NB>
 cudaError_t build(int64_t ne, int64_t nv, const int32_t* cells, cudaStream_t st, PlanDevice* P, int64_t* bad_out)
 {
   const int64_t ngroups = (nv + 31) / 32;
-  unsigned long long* bad = nullptr;  // [0] bad id cell, [1] repeated-vertex cell, [2] degree vertex
-  long long *cnt = nullptr, *v2e_ptr = nullptr, *deg = nullptr, *gw = nullptr;
-  uint32_t* v2e = nullptr;
+  // temporaries, and on failure the plan arrays too, are freed on every exit
+  // path (an FB_TRY return included)
+  struct Scratch {
+    cudaStream_t st;
+    PlanDevice* P;
+    bool ok = false;
+    unsigned long long* bad = nullptr;  // [0] bad id cell, [1] repeated-vertex cell, [2] degree vertex
+    long long *cnt = nullptr, *v2e_ptr = nullptr, *deg = nullptr, *gw = nullptr;
+    uint32_t* v2e = nullptr;
+    ~Scratch()
+    {
+      for (void* q : {(void*)bad, (void*)cnt, (void*)v2e_ptr, (void*)deg, (void*)gw, (void*)v2e})
+        if (q)
+          cudaFreeAsync(q, st);
+      if (!ok)
+      {
+        for (void* q : {(void*)P->goff, (void*)P->spk, (void*)P->spos, (void*)P->nbr_ptr, (void*)P->nbr})
+          if (q)
+            cudaFreeAsync(q, st);
+        *P = PlanDevice{};
+      }
+      cudaStreamSynchronize(st);
+    }
+  } T{st, P};
+  unsigned long long*& bad = T.bad;
+  long long *&cnt = T.cnt, *&v2e_ptr = T.v2e_ptr, *&deg = T.deg, *&gw = T.gw;
+  uint32_t*& v2e = T.v2e;
   FB_TRY(cudaMallocAsync(reinterpret_cast<void**>(&bad), 3 * sizeof(long long), st));
   FB_TRY(cudaMemsetAsync(bad, 0xff, 3 * sizeof(long long), st));
   FB_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), (nv + 1) * sizeof(long long), st));
@@ -235,8 +259,7 @@ cudaError_t build(int64_t ne, int64_t nv, const int32_t* cells, cudaStream_t st,
   FB_TRY(cudaStreamSynchronize(st));
   if (hbad[0] != ~0ull || hbad[1] != ~0ull)
   {
-    cudaFreeAsync(bad, st);
-    cudaFreeAsync(cnt, st);
+    T.ok = true;  // nothing allocated for the plan yet
     bad_out[0] = hbad[0] != ~0ull ? static_cast<int64_t>(hbad[0]) : -1;
     bad_out[1] = hbad[1] != ~0ull ? static_cast<int64_t>(hbad[1]) : -1;
     return cudaSuccess;
@@ -282,13 +305,8 @@ cudaError_t build(int64_t ne, int64_t nv, const int32_t* cells, cudaStream_t st,
                                                    P->spos);
   }
   FB_TRY(cudaGetLastError());
-  cudaFreeAsync(bad, st);
-  cudaFreeAsync(cnt, st);
-  cudaFreeAsync(v2e_ptr, st);
-  cudaFreeAsync(v2e, st);
-  cudaFreeAsync(deg, st);
-  cudaFreeAsync(gw, st);
   FB_TRY(cudaStreamSynchronize(st));
+  T.ok = true;
   launch_counter().fetch_add(nv > 0 ? 5 : 1, std::memory_order_relaxed);
   return cudaSuccess;
 }

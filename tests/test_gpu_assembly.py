@@ -118,6 +118,28 @@ def test_gpu_built_plan_rejects_bad_connectivity():
         fb.AssemblyPlan("elasticity", 3, torch.from_numpy(rep).cuda(), nv)
 
 
+@pytest.mark.parametrize("ids,kind", [((5, 5, -7, 9), "repeated vertex"),     # slot 1 repeats before slot 2 is bad
+                                      ((5, -7, 5, 9), "out of range"),        # slot 1 bad before slot 2 repeats
+                                      ((11, 4, 11, 10 ** 6), "repeated vertex")])
+def test_gpu_and_host_builders_report_the_same_error(ids, kind, monkeypatch):
+    """Both plan builders report the lowest bad cell with the failure the host
+    builder meets first in slot order, whatever mixes in the cell."""
+    import torch
+
+    v, c = fb.structured_mesh(3, 2)
+    nv = v.size // 3
+    bad = c.copy()
+    bad[4 * 6:4 * 7] = ids
+    bad[4 * 9 + 1] = nv + 3  # a later bad cell must not win
+    msgs = []
+    for cells in (bad, torch.from_numpy(bad).cuda()):
+        with pytest.raises(_lib.InvalidArgument) as ei:
+            fb.AssemblyPlan("laplacian", 3, cells, nv)
+        assert ei.value.cell == 6 and kind in str(ei.value)
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]
+
+
 def _raise(plan, var, store):  # fb_assemble with an unknown flag bit
     err = _lib.fb_error()
     rc = plan._lib.fb_assemble(plan._h, var.handle, store.ctypes.data, store.size,

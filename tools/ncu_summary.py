@@ -12,7 +12,13 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.per_cycle_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__occupancy_limit_registers",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-        "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "launch__shared_mem_per_block_dynamic"]
+        "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "launch__shared_mem_per_block_dynamic",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed_op_shared_st.sum",
+        "smsp__inst_executed_op_shared_ld.sum", "smsp__inst_executed_op_global_ld.sum",
+        "smsp__inst_executed_op_global_st.sum"]
 
 
 def ncu(path, *args):

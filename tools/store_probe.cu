@@ -90,6 +90,96 @@ __global__ void __launch_bounds__(128) bulk_cta(char* out, long long ntiles)
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// The fused kernel's shape: every tile, each lane issues gathers for the
+// NEXT tile (L loads, consumed one tile later), writes its S/32 bytes of the
+// tile into staging smem (STS.128), then (FENCE) fence.proxy.async and lane 0
+// issues the 1D bulk store -- or (!BULK) the warp copies LDS.128 -> STG.128.
+// Question: does the proxy fence wait for the outstanding gathers?
+template <int S, bool BULK, bool FENCE, int L>
+__global__ void __launch_bounds__(128) pipe_tile(char* out, const double* src, long long nsrc, long long ntiles,
+                                                 double* sink)
+{
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* mb = sm + warp * 2 * S;
+  const long long stride = (long long)gridDim.x * 4;
+  double acc = 0.0;
+  double nxt[L];
+  long long t = (long long)blockIdx.x * 4 + warp;
+  auto gather = [&](long long tt)
+  {
+#pragma unroll
+    for (int k = 0; k < L; ++k)
+    {
+      const unsigned long long h = (unsigned long long)(tt * 32 + lane) * 0x9E3779B97F4A7C15ull + k * 977;
+      nxt[k] = __ldg(src + (long long)((tt * 32 + lane) * 3 + (h >> 60)) % nsrc);
+    }
+  };
+  gather(t);
+  int it = 0;
+  for (; t < ntiles; t += stride, ++it)
+  {
+    double cur[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k)
+      cur[k] = nxt[k];
+    if (t + stride < ntiles)
+      gather(t + stride);  // next tile's loads in flight
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < L; ++k)
+      v += (float)cur[k];
+    acc += v;
+    unsigned char* buf = mb + (BULK ? (it & 1) * S : 0);
+    if (BULK && it >= 2)
+    {
+      if (lane == 0)
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < S / 512; ++c)
+    {
+      const unsigned a = smem_u32(buf + (c * 32 + lane) * 16);
+      asm volatile("st.shared.v4.f32 [%0], {%1,%1,%1,%1};" ::"r"(a), "f"(v) : "memory");
+    }
+    if (BULK)
+    {
+      if (FENCE)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+      {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t * S),
+                     "r"(smem_u32(buf)), "r"(S)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    else
+    {
+      __syncwarp();
+      float4* o = reinterpret_cast<float4*>(out + t * S);
+#pragma unroll
+      for (int c = 0; c < S / 512; ++c)
+      {
+        float4 q;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+                     : "r"(smem_u32(buf + (c * 32 + lane) * 16)));
+        asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(o + c * 32 + lane), "f"(q.x), "f"(q.y),
+                     "f"(q.z), "f"(q.w)
+                     : "memory");
+      }
+      __syncwarp();
+    }
+  }
+  if (BULK && lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (acc == 12345.0)
+    sink[0] = acc;
+}
+
 // warp block copy LDS.128 -> STG.128 (S bytes per warp tile)
 template <int S>
 __global__ void __launch_bounds__(128) copy_warp(float4* out, long long ntiles)
@@ -200,12 +290,39 @@ void run_copy(char* out, int sms)
   }
 }
 
+template <bool BULK, bool FENCE>
+void run_pipe(char* out, const double* src, long long nsrc, double* sink, int sms, const char* name)
+{
+  constexpr int S = 2048, L = 12;
+  for (int per : {4, 8})
+  {
+    const size_t smem = 4 * 2 * S;
+    cudaFuncSetAttribute(pipe_tile<S, BULK, FENCE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const long long nt = kBytes / 4 / S;  // 1 GiB of output
+    float ms = time_it([&] { pipe_tile<S, BULK, FENCE, L><<<sms * per, 128, smem>>>(out, src, nsrc, nt, sink); });
+    std::printf("pipe %-22s S=%d L=%d ctas/SM=%d  %7.1f GB/s of output\n", name, S, L, per,
+                (kBytes / 4) / (ms * 1e-3) * 1e-9);
+  }
+}
+
 int main()
 {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   char* out = nullptr;
   CK(cudaMalloc(&out, kBytes));
+  {
+    const long long nsrc = 8ll << 20;  // 64 MB of doubles (L2-resident gathers)
+    double* src = nullptr;
+    double* sink = nullptr;
+    CK(cudaMalloc(&src, nsrc * 8));
+    CK(cudaMalloc(&sink, 8));
+    CK(cudaMemset(src, 0, nsrc * 8));
+    run_pipe<false, false>(out, src, nsrc, sink, sms, "copy LDS/STG");
+    run_pipe<true, true>(out, src, nsrc, sink, sms, "bulk + proxy fence");
+    run_pipe<true, false>(out, src, nsrc, sink, sms, "bulk, no fence (racy)");
+    cudaFree(src);
+  }
   for (int per : {4, 8, 16})
   {
     float ms = time_it([&] { regs_store<<<sms * per, 128>>>(reinterpret_cast<float4*>(out), kBytes / 16); });
