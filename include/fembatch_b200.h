@@ -271,8 +271,15 @@ int fb_assembly_pattern(const fb_assembly* a, int64_t* row_ptr, int64_t row_ptr_
 /* flags: FB_ASSEMBLE_SYMMETRIC = the caller promises every element matrix
  * in the store is bitwise symmetric (true of fb_integrate_mesh output of a
  * variant whose fb_variant_path is 0 or 3); the kernel then reads each
- * needed row as the contiguous column.  Values are identical either way. */
-enum fb_assemble_flags { FB_ASSEMBLE_SYMMETRIC = 1 };
+ * needed row as the contiguous column.
+ * FB_ASSEMBLE_BLOCK_DIAGONAL (elasticity; ignored for one-component forms) =
+ * the caller promises every element matrix is zero off the component
+ * diagonal and its nc diagonal blocks are bitwise equal (true of
+ * fb_integrate_mesh / fb_integrate_packed output of any variant whose
+ * fb_variant_path is not 2: SURVEY 8a row A9); only block (0,0) is read,
+ * 1/nc^2 of the store.  Values are identical either way when the promise
+ * holds. */
+enum fb_assemble_flags { FB_ASSEMBLE_SYMMETRIC = 1, FB_ASSEMBLE_BLOCK_DIAGONAL = 2 };
 /* values[nnz] (engine precision of v).  store/values: host or device
  * pointers (host data is staged through the device of `device`). */
 int fb_assemble(const fb_assembly* a, const fb_variant* v, const void* store, int64_t store_len,

@@ -250,8 +250,11 @@ AssemblyPlan make_assembly_plan(Operator op, const Mesh& mesh);
 // `store` must hold the element matrices of the plan's mesh (e.g. from
 // integrate_mesh); `symmetric` = every element matrix is bitwise symmetric
 // (true for integrate_mesh output of the reference forms), read as columns.
+// `block_diagonal` (elasticity) = every element matrix is zero off the
+// component diagonal with equal diagonal blocks (true for integrate_mesh
+// output of a P1-sparse variant): only block (0,0) of the store is read.
 CsrMatrix assemble_global(const KernelVariant& variant, const AssemblyPlan& plan, const ElementMatrixStore& store,
-                          bool symmetric = false, int device = 0);
+                          bool symmetric = false, int device = 0, bool block_diagonal = false);
 // The same operator straight from packed geometry (fb_assemble_packed): the
 // element matrices are recomputed per incidence and never stored; bitwise
 // assemble_global(integrate_batches(geometry)).  Needs a P1-pattern K.

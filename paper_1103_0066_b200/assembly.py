@@ -22,6 +22,11 @@ from . import _lib as L
 from .engine import KernelVariant, _as, _chk, _is_torch, _numel, _op, _ptr
 
 FB_ASSEMBLE_SYMMETRIC = 1
+FB_ASSEMBLE_BLOCK_DIAGONAL = 2
+
+
+def _flags(symmetric: bool, block_diagonal: bool) -> int:
+    return (FB_ASSEMBLE_SYMMETRIC if symmetric else 0) | (FB_ASSEMBLE_BLOCK_DIAGONAL if block_diagonal else 0)
 
 
 class AssemblyPlan:
@@ -67,12 +72,17 @@ class AssemblyPlan:
                                                   col_idx.ctypes.data, col_idx.size, C.byref(err)), err)
         return row_ptr, col_idx
 
-    def assemble(self, variant: KernelVariant, store, values=None, device: int = 0, symmetric: bool = False):
+    def assemble(self, variant: KernelVariant, store, values=None, device: int = 0, symmetric: bool = False,
+                 block_diagonal: bool = False):
         """CSR values (engine precision) of the element matrices in ``store``.
 
         ``symmetric=True`` promises bitwise-symmetric element matrices (the
         ``integrate_mesh`` output of a variant with ``path`` 0 or 3): rows are
-        then read as contiguous columns.  The values do not depend on it."""
+        then read as contiguous columns.  ``block_diagonal=True`` (elasticity)
+        promises element matrices that are zero off the component diagonal
+        with bitwise-equal diagonal blocks (``integrate_mesh`` output of any
+        variant with ``path`` != 2): only block (0, 0) is read.  The values do
+        not depend on either when the promise holds."""
         store = _as(store, variant.dtype, "store")
         if values is None:
             if _is_torch(store) and store.is_cuda:
@@ -84,17 +94,18 @@ class AssemblyPlan:
         _chk(values, variant.dtype, "values")
         err = L.fb_error()
         rc = self._lib.fb_assemble(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
-                                   _numel(values), FB_ASSEMBLE_SYMMETRIC if symmetric else 0, device,
+                                   _numel(values), _flags(symmetric, block_diagonal), device,
                                    C.byref(err))
         L.raise_for(rc, err)
         return values
 
-    def assemble_async(self, variant: KernelVariant, store, values, stream: int = 0, symmetric: bool = False):
+    def assemble_async(self, variant: KernelVariant, store, values, stream: int = 0, symmetric: bool = False,
+                       block_diagonal: bool = False):
         """Enqueue the assembly kernel on ``stream`` (device tensors only)."""
         _chk(store, variant.dtype, "store"), _chk(values, variant.dtype, "values")
         err = L.fb_error()
         rc = self._lib.fb_assemble_async(self._h, variant.handle, _ptr(store), _numel(store), _ptr(values),
-                                         _numel(values), FB_ASSEMBLE_SYMMETRIC if symmetric else 0,
+                                         _numel(values), _flags(symmetric, block_diagonal),
                                          C.c_void_p(stream), C.byref(err))
         L.raise_for(rc, err)
 

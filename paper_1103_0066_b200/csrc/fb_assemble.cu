@@ -157,12 +157,23 @@ __device__ __forceinline__ void load_row(const S* blk, int i, int cj0, S (&r)[N]
   }
 }
 
-template <class S, int DIM, int NC, bool SYM>
-__global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_kernel(const AsmArgs a)
+// DIAG (elasticity, FB_ASSEMBLE_BLOCK_DIAGONAL): the caller promises every
+// element matrix is block diagonal over the components with equal diagonal
+// blocks (integrate_mesh output of a P1-sparse variant: SURVEY 8a row A9), so
+// only block (0, 0) is read -- 1/nc^2 of the store -- and one accumulator
+// per neighbour serves all nc diagonal entries of the row block; the
+// off-diagonal entries are written as +0, exactly the element-order sum of
+// the +0 entries the generic kernel would read.
+template <class S, int DIM, int NC, bool DIAG>
+using AsmShapeOf = AsmShape<S, DIM, DIAG ? 1 : NC>;
+
+template <class S, int DIM, int NC, bool SYM, bool DIAG>
+__global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS) fb_assemble_kernel(const AsmArgs a)
 {
-  using Sh = AsmShape<S, DIM, NC>;
+  using Sh = AsmShapeOf<S, DIM, NC, DIAG>;
   constexpr int NB = DIM + 1, KROWS = NB * NC, NK = KROWS * KROWS;
-  constexpr int NCW = Sh::NCW, NWC = NC / NCW;  // column components per warp, warps per row
+  constexpr int NCW = Sh::NCW, NWC = DIAG ? 1 : NC / NCW;  // column components per warp, warps per row
+  constexpr int TPG = DIAG ? 1 : NC * NWC;                  // tasks (warps) per vertex group
   constexpr int T = 32 * Sh::WARPS;
   constexpr int SLOTS = Sh::SLOTS;
   constexpr int U = Sh::U;
@@ -172,7 +183,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   const S* store = static_cast<const S*>(a.store);
   const int lane = threadIdx.x & 31;
   const int64_t ngroups = (a.nv + 31) / 32;
-  const int64_t nwarps = ngroups * NC * NWC;
+  const int64_t nwarps = ngroups * TPG;
   // task descriptors (row-block offsets of the lane's vertex, the group's
   // plan range) are prefetched one task ahead, so a task's dependent chain
   // is plan -> element rows -> adds, not offsets -> plan -> rows -> adds
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   auto load_desc = [&](int64_t w)
   {
     Desc d;
-    const int64_t g = w / (NC * NWC);
+    const int64_t g = w / TPG;
     const int64_t v = g * 32 + lane;
     if (v < a.nv)
     {
@@ -218,9 +229,9 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
     Desc nxt;
     if (w + wstride < nwarps)
       nxt = load_desc(w + wstride);
-    const int64_t g = w / (NC * NWC);
-    const int sub = static_cast<int>(w - g * (NC * NWC));
-    const int ci = sub / NWC, cj0 = (sub % NWC) * NCW;
+    const int64_t g = w / TPG;
+    const int sub = static_cast<int>(w - g * TPG);
+    const int ci = DIAG ? 0 : sub / NWC, cj0 = DIAG ? 0 : (sub % NWC) * NCW;
     const int64_t r0 = cur.r0;
     const int deg = static_cast<int>(cur.r1 - cur.r0);
     const int64_t q0 = cur.q0, q1 = cur.q1;
@@ -237,7 +248,7 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
         acc[k * T] = S(0);
     else
       for (int k = 0; k < deg; ++k)
-        for (int c = 0; c < NCW; ++c)
+        for (int c = 0; c < (DIAG ? NC : NCW); ++c)
           vals[row + k * NC + c] = S(0);
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
@@ -321,7 +332,24 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
         pk_task = q + 32 * U < q1 ? w : -1;
       }
     }
-    if (in_smem)
+    if constexpr (DIAG)
+    {
+      // row blocks ci = 0 .. nc-1 of the vertex: (k, cj) = acc_k on cj == ci
+      const int64_t r00 = r0 * NC * NC;
+      for (int cr = (in_smem ? 0 : 1); cr < NC; ++cr)
+      {
+        int p = 0;
+        write_seq<S, sizeof(S) == 8 ? 32 : 16>(vals + r00 + static_cast<int64_t>(cr) * deg * NC, deg * NC,
+                                               [&]()
+                                               {
+                                                 const int k = p / NC, cj = p - k * NC;
+                                                 ++p;
+                                                 return cj == cr ? (in_smem ? acc[k * T] : vals[r00 + k * NC])
+                                                                 : S(0);
+                                               });
+      }
+    }
+    else if (in_smem)
     {
       if constexpr (NCW == NC && FB_ASM_VECST)
         write_run<S, T>(vals + row, deg * NC, acc);  // the whole (v, ci) row: contiguous
@@ -334,29 +362,32 @@ __global__ void __launch_bounds__(32 * AsmShape<S, DIM, NC>::WARPS) fb_assemble_
   }
 }
 
-template <class S, int DIM, int NC, bool SYM>
+template <class S, int DIM, int NC, bool SYM, bool DIAG>
 cudaError_t go(const AsmArgs& a, cudaStream_t st)
 {
-  constexpr int T = 32 * AsmShape<S, DIM, NC>::WARPS;
-  const int64_t nwarps = (a.nv + 31) / 32 * NC * (NC / AsmShape<S, DIM, NC>::NCW);
+  using Sh = AsmShapeOf<S, DIM, NC, DIAG>;
+  constexpr int T = 32 * Sh::WARPS;
+  const int64_t nwarps = (a.nv + 31) / 32 * (DIAG ? 1 : NC * (NC / Sh::NCW));
   if (nwarps <= 0)
     return cudaSuccess;
-  // resident CTAs per SM x SMs, computed once per instantiation (reentrant:
-  // concurrent first calls compute the same value)
-  static std::atomic<int> grid_cap_cache{0};
-  int grid_cap = grid_cap_cache.load(std::memory_order_relaxed);
-  if (grid_cap == 0)
-  {
-    int blocks = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_kernel<S, DIM, NC, SYM>, T, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_cap = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
-    grid_cap_cache.store(grid_cap, std::memory_order_relaxed);
-  }
+  // resident CTAs per SM x SMs, computed once per instantiation and device
+  // (fb_devcache.h; reentrant: concurrent first calls compute the same value)
+  static PerDevice grid_cap_cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int grid_cap = grid_cap_cache.get(
+      dev,
+      [&]
+      {
+        int blocks = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_kernel<S, DIM, NC, SYM, DIAG>, T, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
+      },
+      device_setup_counters());
   const int64_t need = (nwarps + T / 32 - 1) / (T / 32);
   const unsigned grid = static_cast<unsigned>(need < grid_cap ? need : grid_cap);
-  fb_assemble_kernel<S, DIM, NC, SYM><<<grid, T, 0, st>>>(a);
+  fb_assemble_kernel<S, DIM, NC, SYM, DIAG><<<grid, T, 0, st>>>(a);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -364,7 +395,10 @@ cudaError_t go(const AsmArgs& a, cudaStream_t st)
 template <class S, int DIM, int NC>
 cudaError_t go_sym(const AsmArgs& a, cudaStream_t st)
 {
-  return a.sym ? go<S, DIM, NC, true>(a, st) : go<S, DIM, NC, false>(a, st);
+  if constexpr (NC > 1)
+    if (a.diag)
+      return a.sym ? go<S, DIM, NC, true, true>(a, st) : go<S, DIM, NC, false, true>(a, st);
+  return a.sym ? go<S, DIM, NC, true, false>(a, st) : go<S, DIM, NC, false, false>(a, st);
 }
 
 }  // namespace

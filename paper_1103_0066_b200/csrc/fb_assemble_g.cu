@@ -392,19 +392,21 @@ cudaError_t go_g(const AsmArgs& a, const KParamBlob& kb, cudaStream_t st)
   const int64_t nwarps = (a.nv + 31) / 32;
   if (nwarps <= 0)
     return cudaSuccess;
-  // resident CTAs per SM x SMs, computed once per instantiation (reentrant:
-  // concurrent first calls compute the same value)
-  static std::atomic<int> grid_cap_cache{0};
-  int grid_cap = grid_cap_cache.load(std::memory_order_relaxed);
-  if (grid_cap == 0)
-  {
-    int blocks = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_g_kernel<S, DIM, OP, MODE, UNI>, T, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_cap = (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
-    grid_cap_cache.store(grid_cap, std::memory_order_relaxed);
-  }
+  // resident CTAs per SM x SMs, computed once per instantiation and device
+  // (fb_devcache.h; reentrant: concurrent first calls compute the same value)
+  static PerDevice grid_cap_cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int grid_cap = grid_cap_cache.get(
+      dev,
+      [&]
+      {
+        int blocks = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fb_assemble_g_kernel<S, DIM, OP, MODE, UNI>, T, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return (blocks > 0 ? blocks : 1) * (sms > 0 ? sms : 1);
+      },
+      device_setup_counters());
   const int64_t need = (nwarps + T / 32 - 1) / (T / 32);
   const unsigned grid = static_cast<unsigned>(need < grid_cap ? need : grid_cap);
   const KP<S, DIM, OP>& kp = *reinterpret_cast<const KP<S, DIM, OP>*>(kb.bytes);

@@ -333,7 +333,7 @@ void check_pair(const fb_assembly* a, const fb_variant* v, int64_t store_len, in
 
 void check_flags(int flags)
 {
-  if (flags & ~FB_ASSEMBLE_SYMMETRIC)
+  if (flags & ~(FB_ASSEMBLE_SYMMETRIC | FB_ASSEMBLE_BLOCK_DIAGONAL))
     invalid("unknown assembly flags");
 }
 
@@ -351,6 +351,7 @@ void launch_on(const fb_assembly& A, const fb_variant& v, const void* store, voi
   g.nv = A.nv;
   // column reads need the caller's symmetry promise and 16-byte alignment
   g.sym = (flags & FB_ASSEMBLE_SYMMETRIC) && (reinterpret_cast<uintptr_t>(store) & 15u) == 0 ? 1 : 0;
+  g.diag = (flags & FB_ASSEMBLE_BLOCK_DIAGONAL) && A.nc > 1 ? 1 : 0;
   cuda_check(fbk::launch_assemble(A.dim, A.nc, v.cfg.precision, g, st), "assemble kernel launch");
 }
 

@@ -83,6 +83,8 @@ struct AsmArgs {
   void* values = nullptr;           // CSR values (engine precision)
   int64_t nv = 0;
   int sym = 0;                      // element matrices bitwise symmetric: read columns
+  int diag = 0;                     // elasticity: block-diagonal element matrices with equal
+                                    // diagonal blocks (read block (0,0) only)
   // G-input assembly (fb_assemble_g.cu): element rows recomputed from the
   // packed geometry (PackedGeometry layout) instead of read from a store
   const void* g_in = nullptr;

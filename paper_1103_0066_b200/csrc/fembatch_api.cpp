@@ -681,7 +681,7 @@ AssemblyPlan make_assembly_plan(Operator op, const Mesh& mesh)
 }
 
 CsrMatrix assemble_global(const KernelVariant& v, const AssemblyPlan& plan, const ElementMatrixStore& store,
-                          bool symmetric, int device)
+                          bool symmetric, int device, bool block_diagonal)
 {
   if (!v.device || !plan.device)
     throw std::invalid_argument("variant or assembly plan was not created for the GPU");
@@ -698,7 +698,8 @@ CsrMatrix assemble_global(const KernelVariant& v, const AssemblyPlan& plan, cons
   m.values = make_scalar_array(store.precision, plan.nnz);
   check(fb_assemble(plan.device.get(), v.device.get(), data_ptr(store.data),
                     scalar_array_size(store.data), data_ptr(m.values), plan.nnz,
-                    symmetric ? FB_ASSEMBLE_SYMMETRIC : 0, device, &err),
+                    (symmetric ? FB_ASSEMBLE_SYMMETRIC : 0) | (block_diagonal ? FB_ASSEMBLE_BLOCK_DIAGONAL : 0),
+                    device, &err),
         err);
   return m;
 }

@@ -39,15 +39,17 @@ def test_assembly_bitwise_vs_oracle(restatement, op, dim, n, prec):
     want = restatement.assemble(op, dim, c, nv, prec, want_store, rp, ci)
     assert var.path in (0, 3)  # symmetric kernel path: element matrices bitwise symmetric
     for sym in (False, True):
-        got_host = plan.assemble(var, store, symmetric=sym)
-        assert got_host.tobytes() == want.tobytes()
-        dstore = torch.from_numpy(store).cuda()
-        got_dev = plan.assemble(var, dstore, symmetric=sym)
-        assert got_dev.is_cuda and got_dev.cpu().numpy().tobytes() == want.tobytes()
-        vals = torch.full((plan.nnz,), float("nan"), dtype=dstore.dtype, device="cuda")
-        plan.assemble_async(var, dstore, vals, torch.cuda.current_stream().cuda_stream, symmetric=sym)
-        torch.cuda.synchronize()
-        assert vals.cpu().numpy().tobytes() == want.tobytes()
+        for diag in (False, True):  # block-diagonal promise (elasticity; a no-op otherwise)
+            got_host = plan.assemble(var, store, symmetric=sym, block_diagonal=diag)
+            assert got_host.tobytes() == want.tobytes()
+            dstore = torch.from_numpy(store).cuda()
+            got_dev = plan.assemble(var, dstore, symmetric=sym, block_diagonal=diag)
+            assert got_dev.is_cuda and got_dev.cpu().numpy().tobytes() == want.tobytes()
+            vals = torch.full((plan.nnz,), float("nan"), dtype=dstore.dtype, device="cuda")
+            plan.assemble_async(var, dstore, vals, torch.cuda.current_stream().cuda_stream, symmetric=sym,
+                                block_diagonal=diag)
+            torch.cuda.synchronize()
+            assert vals.cpu().numpy().tobytes() == want.tobytes()
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
@@ -293,6 +295,22 @@ def test_packed_assembly_high_degree_and_general_k(restatement, op, dim, prec):
     want, got = _packed_case(var, op, dim, v, c, prec, 8)
     assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
     del torch
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_block_diagonal_store_assembly_hub_vertices(restatement, dim, prec):
+    """Block-diagonal reads with hub vertices beyond the shared-memory slots
+    (accumulated in the output rows, then expanded over the components)."""
+    v, c = fan_mesh(dim, 40)
+    nv = v.size // dim
+    var = fb.make_variant("elasticity", dim, prec, "strict", element_batch_size=8)
+    store = fb.integrate_mesh(var, v, c)
+    plan = fb.AssemblyPlan("elasticity", dim, c, nv)
+    rp, ci = plan.pattern()
+    want = restatement.assemble("elasticity", dim, c, nv, prec, store, rp, ci)
+    for sym in (False, True):
+        assert plan.assemble(var, store, symmetric=sym, block_diagonal=True).tobytes() == want.tobytes()
 
 
 def test_packed_assembly_validation(restatement):

@@ -71,30 +71,35 @@ def main():
             fb.integrate_mesh_async(var, dv, dc, store, st, sid)
             fb.status_check(st, sid)
             vals = torch.empty(plan.nnz, device="cuda", dtype=store.dtype)
-            for _ in range(3):
-                plan.assemble_async(var, store, vals, sid, symmetric=True)
-            ms = []
-            for _ in range(a.steps):
-                scrub.view(torch.int64).sum()
-                torch.cuda._sleep(bench.GAP_CYCLES)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                plan.assemble_async(var, store, vals, sid, symmetric=True)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ms.append(e0.elapsed_time(e1))
-            t = statistics.median(ms)
-            by = ne * nb * (4 + nb) + 2 * 8 * (nv + 1) + ne * kr * kr * s + plan.nnz * s
-            r = {"workload": w, "kernel": "fb_assemble_kernel", "op": op, "dim": dim, "prec": prec,
-                 "elements": ne, "rows": plan.rows, "nnz": plan.nnz, "ms": round(t, 4),
-                 "algorithmic_bytes": by, "GBs": round(by / (t * 1e-3) * 1e-9),
-                 "frac": round(by / (t * 1e-3) * 1e-9 / peak, 3), "peak_GBs": peak, "peak_source": peak_src,
-                 "Gnnz_s": round(plan.nnz / (t * 1e-3) * 1e-9, 2),
-                 "Gelem_s": round(ne / (t * 1e-3) * 1e-9, 2), "plan_build_gpu_s": round(t_plan, 4),
-                 "plan_build_host_s": round(t_plan_host, 3),
-                 "plan_build_from_host_cells_s": round(t_plan_hostcells, 4)}
-            print(json.dumps(r), flush=True)
-            res.append(r)
+            # elasticity also with the block-diagonal promise (SURVEY 8a row A9:
+            # only block (0,0) of each element matrix is read)
+            for diag in ((False, True) if op == "elasticity" else (False,)):
+                for _ in range(3):
+                    plan.assemble_async(var, store, vals, sid, symmetric=True, block_diagonal=diag)
+                ms = []
+                for _ in range(a.steps):
+                    scrub.view(torch.int64).sum()
+                    torch.cuda._sleep(bench.GAP_CYCLES)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    plan.assemble_async(var, store, vals, sid, symmetric=True, block_diagonal=diag)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                t = statistics.median(ms)
+                read_scalars = nb * nb if diag else kr * kr
+                by = ne * nb * (4 + nb) + 2 * 8 * (nv + 1) + ne * read_scalars * s + plan.nnz * s
+                r = {"workload": w, "kernel": "fb_assemble_kernel" + (" (block diagonal)" if diag else ""),
+                     "op": op, "dim": dim, "prec": prec,
+                     "elements": ne, "rows": plan.rows, "nnz": plan.nnz, "ms": round(t, 4),
+                     "algorithmic_bytes": by, "GBs": round(by / (t * 1e-3) * 1e-9),
+                     "frac": round(by / (t * 1e-3) * 1e-9 / peak, 3), "peak_GBs": peak, "peak_source": peak_src,
+                     "Gnnz_s": round(plan.nnz / (t * 1e-3) * 1e-9, 2),
+                     "Gelem_s": round(ne / (t * 1e-3) * 1e-9, 2), "plan_build_gpu_s": round(t_plan, 4),
+                     "plan_build_host_s": round(t_plan_host, 3),
+                     "plan_build_from_host_cells_s": round(t_plan_hostcells, 4)}
+                print(json.dumps(r), flush=True)
+                res.append(r)
             # assembly straight from packed G (no element store), and the two
             # mesh -> CSR pipelines: integrate + assemble vs pack + assemble_packed
             g = torch.empty(var.store_length(ne) // (kr * kr) * dim * dim, device="cuda", dtype=store.dtype)
@@ -119,7 +124,8 @@ def main():
             tp = timed(lambda: plan.assemble_packed_async(var, g, pv, None, sid))
             assert torch.equal(pv, vals), "packed assembly differs from the store assembly"
             t_store_path = timed(lambda: (fb.integrate_mesh_async(var, dv, dc, store, st, sid),
-                                          plan.assemble_async(var, store, vals, sid, symmetric=True)))
+                                          plan.assemble_async(var, store, vals, sid, symmetric=True,
+                                                              block_diagonal=op == "elasticity")))
             t_packed_path = timed(lambda: (fb.pack_geometry_async(dv, dc, dim, g, st, var.config.element_batch_size,
                                                                   prec, sid),
                                            plan.assemble_packed_async(var, g, pv, None, sid)))
