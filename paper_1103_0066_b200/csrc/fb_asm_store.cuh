@@ -85,4 +85,39 @@ __device__ __forceinline__ void write_seq(S* base, int64_t len, F&& next)
     base[p] = next();
 }
 
+
+#ifndef FB_ASMG_VECST
+#define FB_ASMG_VECST 1
+#endif
+// Write-out of a vertex's CSR row block (nc rows x deg*nc entries,
+// contiguous, ci-major): entry (ci, k, cj) = acc[k] on the diagonal
+// (cj == ci), +0 elsewhere, written with full-sector vector stores
+// (fb_asm_store.cuh).  acc reads are the lane's own shared-memory column
+// ([slot][thread]): conflict-free for any k.
+template <class S, int NC, int T, bool VEC = true>
+__device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
+{
+  const int64_t len = static_cast<int64_t>(deg) * NC * NC;
+  int ci = 0, k = 0, cj = 0;
+  auto next = [&]() -> S
+  {
+    const S x = cj == ci ? acc[k * T] : S(0);
+    if (++cj == NC)
+    {
+      cj = 0;
+      if (++k == deg)
+      {
+        k = 0;
+        ++ci;
+      }
+    }
+    return x;
+  };
+  if (VEC)
+    write_seq<S, 32>(base, len, next);  // A/B: 16-byte stores 0.56 -> 0.43 ms (3D-E f32)
+  else
+    for (int64_t p = 0; p < len; ++p)
+      base[p] = next();
+}
+
 }  // namespace fbk

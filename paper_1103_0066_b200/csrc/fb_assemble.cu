@@ -246,9 +246,12 @@ __global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS) fb_a
     if (in_smem)
       for (int k = 0; k < deg * NCW; ++k)
         acc[k * T] = S(0);
+    else if (DIAG)
+      for (int k = 0; k < deg * NC * NC; ++k)  // the whole row block (zeros off the diagonal)
+        vals[row + k] = S(0);
     else
       for (int k = 0; k < deg; ++k)
-        for (int c = 0; c < (DIAG ? NC : NCW); ++c)
+        for (int c = 0; c < NCW; ++c)
           vals[row + k * NC + c] = S(0);
     for (int64_t q = q0 + lane; q < q1; q += 32 * U)
     {
@@ -336,18 +339,15 @@ __global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS) fb_a
     {
       // row blocks ci = 0 .. nc-1 of the vertex: (k, cj) = acc_k on cj == ci
       const int64_t r00 = r0 * NC * NC;
-      for (int cr = (in_smem ? 0 : 1); cr < NC; ++cr)
-      {
-        int p = 0;
-        write_seq<S, sizeof(S) == 8 ? 32 : 16>(vals + r00 + static_cast<int64_t>(cr) * deg * NC, deg * NC,
-                                               [&]()
-                                               {
-                                                 const int k = p / NC, cj = p - k * NC;
-                                                 ++p;
-                                                 return cj == cr ? (in_smem ? acc[k * T] : vals[r00 + k * NC])
-                                                                 : S(0);
-                                               });
-      }
+      if (in_smem)
+        write_block<S, NC, T>(vals + r00, deg, acc);  // one contiguous run, full-sector stores
+      else
+        for (int k = 0; k < deg; ++k)  // ci = 0 accumulated in place; rows ci > 0 were zeroed
+        {
+          const S x = vals[r00 + k * NC];
+          for (int cr = 1; cr < NC; ++cr)
+            vals[r00 + static_cast<int64_t>(cr) * deg * NC + k * NC + cr] = x;
+        }
     }
     else if (in_smem)
     {

@@ -158,40 +158,6 @@ __device__ __forceinline__ void select_row(const S (&vv)[NB * NB], int aa, S (&x
       x[b] = aa == r ? vv[r * NB + b] : x[b];
 }
 
-#ifndef FB_ASMG_VECST
-#define FB_ASMG_VECST 1
-#endif
-// Write-out of a vertex's CSR row block (nc rows x deg*nc entries,
-// contiguous, ci-major): entry (ci, k, cj) = acc[k] on the diagonal
-// (cj == ci), +0 elsewhere, written with full-sector vector stores
-// (fb_asm_store.cuh).  acc reads are the lane's own shared-memory column
-// ([slot][thread]): conflict-free for any k.
-template <class S, int NC, int T>
-__device__ __forceinline__ void write_block(S* base, int deg, const S* acc)
-{
-  const int64_t len = static_cast<int64_t>(deg) * NC * NC;
-  int ci = 0, k = 0, cj = 0;
-  auto next = [&]() -> S
-  {
-    const S x = cj == ci ? acc[k * T] : S(0);
-    if (++cj == NC)
-    {
-      cj = 0;
-      if (++k == deg)
-      {
-        k = 0;
-        ++ci;
-      }
-    }
-    return x;
-  };
-  if (FB_ASMG_VECST)
-    write_seq<S, 32>(base, len, next);  // A/B: 16-byte stores 0.56 -> 0.43 ms (3D-E f32)
-  else
-    for (int64_t p = 0; p < len; ++p)
-      base[p] = next();
-}
-
 #ifndef FB_ASMG_ROW
 #define FB_ASMG_ROW 1
 #endif
@@ -372,7 +338,7 @@ __global__ void __launch_bounds__(32 * GShape<S, DIM, OP>::WARPS)
       }
     }
     if (in_smem)
-      write_block<S, NC, T>(vals + row0, deg, acc);
+      write_block<S, NC, T, FB_ASMG_VECST != 0>(vals + row0, deg, acc);
     else if (NC > 1)
       for (int k = 0; k < deg; ++k)
       {
