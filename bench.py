@@ -538,6 +538,15 @@ def main():
         e2e_ms = max_over_ranks(e2e_ms)
         del hout, hout_np
 
+        # the other arithmetic mode of the same precision (fast: FP64 edges, then
+        # FMA geometry in the engine precision; within the stated tolerances,
+        # tests/test_gpu_parity.py -- not bitwise)
+        omode = "fast" if args.mode == "strict" else "strict"
+        var_m = fb.make_variant(op, dim, prec, omode, element_batch_size=128)
+        ms_m, _, lm = kernel_steps(var_m, dv, dc, out, args.steps, args.warmup)
+        ms_m = max_over_ranks(ms_m)
+        launches += lm
+
         # the other precision of the same config, same mesh
         other = "f64" if prec == "f32" else "f32"
         var2 = fb.make_variant(op, dim, other, args.mode, element_batch_size=128)
@@ -661,6 +670,10 @@ def main():
                 "elements_per_s": ne_per * world / (ms2 * 1e-3),
                 "roofline_frac": bytes2 / (ms2 * 1e-3) * 1e-9 / peak},
         "ms_min": ms_min,
+        f"{prec}_{omode}": {"value": flops / (ms_m * 1e-3) * 1e-9, "unit": "GFLOP/s", "ms_per_step": ms_m,
+                            "roofline_frac": bytes_launch / (ms_m * 1e-3) * 1e-9 / peak,
+                            "parity": ("normwise <= 5e-6 (f32) / 1e-13 (f64) vs the FP64 direct oracle"
+                                       if omode == "fast" else "bitwise the reference")},
         "steady_state": None if steady is None else {
             "ms_per_launch": steady, "value": flops / (steady * 1e-3) * 1e-9,
             "roofline_frac": bytes_launch / (steady * 1e-3) * 1e-9 / peak,

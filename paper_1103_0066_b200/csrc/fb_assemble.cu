@@ -17,6 +17,7 @@
 // (thread-private) rows of the output.
 #include <atomic>
 #include <cstdint>
+#include <type_traits>
 
 #include <cuda_runtime.h>
 
@@ -53,12 +54,23 @@ namespace {
 #ifndef FB_ASM_U2D
 #define FB_ASM_U2D FB_ASM_U
 #endif
+// 16 incidences in flight for the latency-bound 3D elasticity FP64 gather and
+// the 3D block-diagonal reads (A/B r02: 3D-E-8M f64 4.65 -> 4.09 ms, block
+// diagonal f64 0.95 -> 0.89, f32 0.59 -> 0.54; 16 everywhere loses up to 2x
+// on 2D and 3D-L)
+#ifndef FB_ASM_U_3E64
+#define FB_ASM_U_3E64 16
+#endif
+#ifndef FB_ASM_U_DIAG3
+#define FB_ASM_U_DIAG3 16
+#endif
 template <class S, int DIM, int NC>
 struct AsmShape {
   static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : (NC == 3 ? FB_ASM_NCW3D64 : 1));
   static constexpr int WARPS = NCW == 1 ? 4 : FB_ASM_WARPS_NCW;
   static constexpr int SLOTS = NCW == 1 ? 32 : 24;
-  static constexpr int U = DIM == 2 ? FB_ASM_U2D : (NCW == 1 ? FB_ASM_U : 4);
+  static constexpr int U = DIM == 2 ? FB_ASM_U2D
+                           : (NC == 3 && sizeof(S) == 8 ? FB_ASM_U_3E64 : (NCW == 1 ? FB_ASM_U : 4));
   // prefetch the next chunk's plan entries (registers: 3D elasticity FP64,
   // already at the register limit, is faster without -- A/B measured)
   static constexpr bool PREF = !(NC == 3 && sizeof(S) == 8);
@@ -164,8 +176,12 @@ __device__ __forceinline__ void load_row(const S* blk, int i, int cj0, S (&r)[N]
 // per neighbour serves all nc diagonal entries of the row block; the
 // off-diagonal entries are written as +0, exactly the element-order sum of
 // the +0 entries the generic kernel would read.
+template <class S, int DIM>
+struct AsmShapeDiag : AsmShape<S, DIM, 1> {
+  static constexpr int U = DIM == 3 ? FB_ASM_U_DIAG3 : FB_ASM_U2D;  // incidences in flight per lane
+};
 template <class S, int DIM, int NC, bool DIAG>
-using AsmShapeOf = AsmShape<S, DIM, DIAG ? 1 : NC>;
+using AsmShapeOf = std::conditional_t<DIAG, AsmShapeDiag<S, DIM>, AsmShape<S, DIM, NC>>;
 
 template <class S, int DIM, int NC, bool SYM, bool DIAG>
 __global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS) fb_assemble_kernel(const AsmArgs a)

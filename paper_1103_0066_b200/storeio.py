@@ -105,10 +105,13 @@ def _q(s: str) -> str:
     return '"' + s.replace('"', '""') + '"'
 
 
-def write_bench_csv(path: str, records) -> None:
-    """records: dicts keyed by the CSV field names (flags as bools)."""
+def write_bench_csv(path: str, records, extra=()) -> None:
+    """records: dicts keyed by the CSV field names (flags as bools).  `extra`
+    names extension columns appended after the reference's 15 (numbers at 17
+    significant digits, None as an empty cell); with none the file is the
+    reference's format byte for byte."""
     with open(path, "w", newline="") as f:
-        f.write(CSV_HEADER + "\n")
+        f.write(CSV_HEADER + "".join("," + k for k in extra) + "\n")
         for r in records:
             out = []
             for k in _FIELDS:
@@ -121,6 +124,9 @@ def write_bench_csv(path: str, records) -> None:
                     out.append(str(int(v)))
                 else:
                     out.append(_q(str(v)))
+            for k in extra:
+                v = r.get(k)
+                out.append("" if v is None else (str(v) if isinstance(v, int) else _g17(float(v))))
             f.write(",".join(out) + "\n")
 
 

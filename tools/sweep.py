@@ -2,10 +2,14 @@
 for {Laplacian, elasticity} x {2D, 3D} x {f32, f64}, strict mode, on G GPUs of
 this process (the engine's contiguous tile-aligned element shards,
 fb.shard_bounds, one per device, no collectives).  Inputs resident, L2
-flushed between steps.  ms = wall time from a host barrier (all devices idle)
-to the last device's completion, launches issued by one host thread per
-device; ms_device_max = max over devices of the CUDA-event kernel
-time, for reference.  Writes CSV rows to stdout and to
+flushed between steps.  ms = (G > 1) wall time from a host barrier (all
+devices idle) to the last device's completion, launches issued by one host
+thread per device (SURVEY 8d), or (G = 1) the kernel's CUDA-event time;
+ms_device_max = max over devices of the CUDA-event kernel time.  The same
+points are also written in the reference's benchmark-record CSV schema plus
+the SURVEY section 5 extension columns (devices, gbytes_per_s,
+roofline_fraction, ref_cpu_seconds = the reference CPU path on all host
+threads for N <= 2^22, host_cores) to profiles/<out>_records.csv.  Writes CSV rows to stdout and to
 profiles/<out>.csv.
 
     python tools/sweep.py [--gpus G] [--min-log2 12] [--max-log2 28] [--step 2] [--out r01_sweep_1gpu]
@@ -44,7 +48,10 @@ def main():
     p.add_argument("--ops", default="laplacian,elasticity")
     p.add_argument("--dims", default="2,3")
     p.add_argument("--precisions", default="f32,f64")
-    p.add_argument("--out", default="r01_sweep_1gpu")
+    p.add_argument("--out", default="r02_sweep_1gpu")
+    p.add_argument("--ref-max-log2", type=int, default=22,
+                   help="time the reference CPU path (oracle/_ref, all host threads) up to this size")
+    p.add_argument("--checksum-max-log2", type=int, default=24)
     a = p.parse_args()
     peak, _ = bench.peaks()
     G = min(a.gpus, torch.cuda.device_count())
@@ -58,6 +65,16 @@ def main():
     f = open(path, "w", newline="")
     w = csv.DictWriter(f, fieldnames=fields)
     w.writeheader()
+    # the same points in the reference's benchmark-record schema (src/bench.cpp
+    # CSV, 15 columns) plus the extension columns of SURVEY section 5
+    records = []
+    EXT = ("devices", "gbytes_per_s", "roofline_fraction", "ref_cpu_seconds", "host_cores")
+    host_cores = bench.host_cores()
+    try:
+        from oracle.oracle import Reference, reference_available
+        ref = Reference() if reference_available() else None
+    except Exception:
+        ref = None
     sizes = [1 << k for k in range(a.min_log2, a.max_log2 + 1, a.step)]
     for dim in [int(x) for x in a.dims.split(",")]:
         v, c, _ = fb.mesh_prefix(dim, sizes[-1], 0.0, 42)
@@ -70,8 +87,14 @@ def main():
                     kr = bench.krows(op, dim)
                     s = 4 if prec == "f32" else 8
                     row = {"op": op, "dim": dim, "precision": prec, "elements": N, "gpus": G}
+                    rec = {"operator": op, "dim": dim, "num_elements": N, "batch_size": 128, "concurrent": 1,
+                           "interleave": False, "unroll": False, "precision": prec, "workers": G,
+                           "reps": a.steps, "seconds_min": 0.0, "seconds_mean": 0.0, "gflops": 0.0,
+                           "checksum": 0.0, "devices": G, "host_cores": host_cores}
                     if N * kr * kr * s / G > a.max_store_gb * 1e9:
                         row["status"] = "skipped: store exceeds per-GPU budget"
+                        rec["status"] = row["status"]
+                        records.append(rec)
                         w.writerow(row)
                         f.flush()
                         print(row, flush=True)
@@ -121,11 +144,30 @@ def main():
                             t.join()
                         wall = (time.perf_counter() - t0) * 1e3
                         if it >= 2:
-                            times.append(wall)
-                            dev_times.append(max(e0.elapsed_time(e1) for e0, e1 in evs))
+                            dev = max(e0.elapsed_time(e1) for e0, e1 in evs)
+                            # one device: its kernel time (a host wall clock around a
+                            # ~3 us kernel is thread wake-up and launch latency)
+                            times.append(wall if G > 1 else dev)
+                            dev_times.append(dev)
                     for d in range(G):
                         with torch.cuda.device(d):
                             fb.status_check(shards[d][3], torch.cuda.current_stream().cuda_stream)
+                    # checksum: real entries in element order, summed sequentially in double
+                    csum = float("nan")
+                    if N <= (1 << a.checksum_max_log2):
+                        kr2 = kr * kr
+                        tot = 0.0
+                        for d in range(G):
+                            o = shards[d][2][: (b[d + 1] - b[d]) * kr2].double().cpu().numpy()
+                            for q in range(0, o.size, 1 << 24):
+                                cs = np.cumsum(np.concatenate(([tot], o[q:q + (1 << 24)])))
+                                tot = float(cs[-1])
+                        csum = tot
+                    ref_s = None
+                    if ref is not None and N <= (1 << a.ref_max_log2):
+                        ref_s, _ = ref.time_integrate(op, v, cN, dim, bs=128, ce=2, interleave=True,
+                                                      precision=0 if prec == "f32" else 1, workers=host_cores,
+                                                      reps=1, include_packing=True)
                     del shards
                     ms = statistics.median(times)
                     by = N * nb * 4 + nv_ref * dim * 8 + N * kr * kr * s
@@ -138,7 +180,16 @@ def main():
                     w.writerow(row)
                     f.flush()
                     print(row, flush=True)
+                    rec.update(seconds_min=min(times) * 1e-3, seconds_mean=statistics.mean(times) * 1e-3,
+                               gflops=bench.flops_per_element(op, dim) * N / (min(times) * 1e-3) * 1e-9,
+                               checksum=csum, gbytes_per_s=gbs, roofline_fraction=gbs / (peak * G),
+                               ref_cpu_seconds=ref_s, status="ok")
+                    records.append(rec)
     f.close()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    rpath = os.path.join(ROOT, "profiles", a.out + "_records.csv")
+    fb.write_bench_csv(rpath, records, extra=EXT)
+    shutil.copy(rpath, os.path.join(ROOT, "gpurun_out", a.out + "_records.csv"))
     # a copy the GPU-box runner brings back
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     shutil.copy(path, os.path.join(ROOT, "gpurun_out", a.out + ".csv"))
