@@ -87,3 +87,26 @@ def test_bench_csv_reader_rejects_malformed(tmp_path):
         p.write_text(text)
         with pytest.raises(ValueError):
             fb.read_bench_csv(str(p))
+
+
+def test_bench_csv_extension_columns(tmp_path):
+    """The sweep table: the reference's 15 columns byte for byte, then the
+    SURVEY section 5 extension columns (empty cell for a missing value)."""
+    import paper_1103_0066_b200 as fb
+    from paper_1103_0066_b200.storeio import CSV_HEADER
+
+    rec = {"operator": "laplacian", "dim": 3, "num_elements": 4096, "batch_size": 128, "concurrent": 1,
+           "interleave": False, "unroll": False, "precision": "f32", "workers": 1, "reps": 5,
+           "seconds_min": 1.5e-6, "seconds_mean": 2e-6, "gflops": 123.25, "checksum": 0.0, "status": "ok",
+           "devices": 1, "gbytes_per_s": 1000.5, "roofline_fraction": 0.5, "ref_cpu_seconds": None,
+           "host_cores": 16}
+    ext = ("devices", "gbytes_per_s", "roofline_fraction", "ref_cpu_seconds", "host_cores")
+    p = tmp_path / "t.csv"
+    fb.write_bench_csv(str(p), [rec], extra=ext)
+    head, row = p.read_text().splitlines()
+    assert head == CSV_HEADER + ",devices,gbytes_per_s,roofline_fraction,ref_cpu_seconds,host_cores"
+    assert row.endswith(',"ok",1,1000.5,0.5,,16')
+    plain = tmp_path / "p.csv"
+    fb.write_bench_csv(str(plain), [rec])
+    assert plain.read_text().splitlines()[0] == CSV_HEADER
+    assert p.read_text().splitlines()[1].startswith(plain.read_text().splitlines()[1])
