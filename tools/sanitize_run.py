@@ -6,7 +6,8 @@ racecheck / synccheck):
 Covers the fused integration (every op x dim x precision x store path,
 ragged tile counts, unaligned output), GPU pack_geometry, the G-input path,
 the GPU assembly plan build and both assembly kernels (store and packed G,
-incl. hub vertices beyond the shared-memory slots).  Run with
+incl. hub vertices beyond the shared-memory slots, and the block-diagonal
+store reads).  Run with
 PYTORCH_NO_CUDA_MEMORY_CACHING=1 so every buffer is its own allocation.
 """
 import os
@@ -48,8 +49,9 @@ def main():
                 fb.integrate_packed_async(var, g, ne, out, sid, coefficients=coeffs)
                 plan = fb.AssemblyPlan(op, dim, dc, v.size // dim)
                 for sym in (False, True):
-                    vals = torch.empty(plan.nnz, dtype=dt, device="cuda")
-                    plan.assemble_async(var, out, vals, sid, symmetric=sym)
+                    for diag in ((False, True) if op == "elasticity" else (False,)):
+                        vals = torch.empty(plan.nnz, dtype=dt, device="cuda")
+                        plan.assemble_async(var, out, vals, sid, symmetric=sym, block_diagonal=diag)
                 # assembly from packed G: G of exactly ne*dim^2 scalars (the
                 # vector loads' tail guard), aligned and misaligned
                 gx = torch.empty(ne * dim * dim + 1, dtype=dt, device="cuda")
@@ -76,6 +78,8 @@ def main():
                 plan = fb.AssemblyPlan(op, dim, dc, v.size // dim)
                 vals = torch.empty(plan.nnz, dtype=dt, device="cuda")
                 plan.assemble_async(var, out, vals, sid, symmetric=True)
+                if op == "elasticity":
+                    plan.assemble_async(var, out, vals, sid, symmetric=True, block_diagonal=True)
                 plan.assemble_packed_async(var, g, vals, None, sid)
                 torch.cuda.synchronize()
     print("sanitize run ok")
