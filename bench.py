@@ -399,6 +399,11 @@ def main():
     args = parse()
     rank, world, local = dist_env()
     if world == 1 and args.gpus > 1:
+        if args.impl != "reference" and os.environ.get("FB_BENCH_SHARED_GPU") != "1":
+            import torch
+
+            if torch.cuda.device_count() < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs; {torch.cuda.device_count()} visible")
         sys.exit(spawn_ranks(args))
     if world > 1 and args.gpus != world:
         sys.exit(f"bench.py: --gpus {args.gpus} but torchrun started {world} ranks")

@@ -22,9 +22,18 @@ def main():
     p.add_argument("--mode", default="strict")
     p.add_argument("--store", default="auto")
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--elements", type=int, default=0, help="override the workload's element count")
+    p.add_argument("--op", default="", help="override the workload's operator")
     a = p.parse_args()
     op, dim, ne, _ = bench.WORKLOADS[a.workload]
-    v, c, _ = bench.build_rank_mesh(op, dim, ne, 0, 1)
+    op = a.op or op
+    ne = a.elements or ne
+    from paper_1103_0066_b200 import mesh_prefix
+    v, c, _ = mesh_prefix(dim, ne, 0.15 if ne <= (1 << 24) else 0.0, 42)
+    w = None
+    if op == "weighted-laplacian":
+        import numpy as np
+        w = torch.from_numpy(np.ascontiguousarray(1.0 + v.reshape(-1, dim)[c.reshape(-1, dim + 1), 0].ravel())).cuda()
     var = fb.make_variant(op, dim, a.precision, a.mode, element_batch_size=128, store=a.store)
     dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
     out = torch.empty(var.store_length(ne), dtype=torch.float32 if a.precision == "f32" else torch.float64,
@@ -33,7 +42,7 @@ def main():
     sid = torch.cuda.current_stream().cuda_stream
     fb.status_reset(st, sid)
     for _ in range(a.reps):
-        fb.integrate_mesh_async(var, dv, dc, out, st, sid)
+        fb.integrate_mesh_async(var, dv, dc, out, st, sid, coefficients=w)
     fb.status_check(st, sid)
     torch.cuda.synchronize()
     print("ok", a)
