@@ -66,3 +66,29 @@ def test_gpus_flag_is_not_silently_ignored():
     out = r.stdout.strip()
     assert r.returncode != 0
     assert '"n_gpus": 1' not in out
+
+
+def test_committed_traffic_is_keyed_to_the_kernel_sources(tmp_path, monkeypatch):
+    """roofline.traffic comes from an ncu capture of the CURRENT kernel
+    sources only; a capture of other sources reads as stale (None)."""
+    import json as _json
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    sha = bench.kernel_source_sha()
+    assert len(sha) == 16
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    (prof / "ncu_traffic.json").write_text(_json.dumps({
+        "w:f32:strict": {"traffic": 123.0, "kernel_sha": sha, "report": "x.ncu-rep"},
+        "w:f64:strict": {"traffic": 456.0, "kernel_sha": "0" * 16, "report": "y.ncu-rep"},
+        "w:f32:fast": 789.0}))
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    # kernel_source_sha reads the sources under ROOT: keep the real ones
+    monkeypatch.setattr(bench, "kernel_source_sha", lambda: sha)
+    assert bench.committed_traffic("w", "f32", "strict") == (123.0, "x.ncu-rep")
+    t, why = bench.committed_traffic("w", "f64", "strict")
+    assert t is None and "stale" in why
+    assert bench.committed_traffic("w", "f32", "fast")[0] is None
+    assert bench.committed_traffic("nope", "f32", "strict")[0] is None
