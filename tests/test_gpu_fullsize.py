@@ -137,3 +137,26 @@ def test_fast_mode_at_size_against_direct_oracle(restatement, op, dim, ne, prec,
     a = got.reshape(-1, kr, kr).transpose(0, 2, 1)
     direct = restatement.direct_mesh(op, v, c, dim, elements=idx)
     assert normwise_error(a, direct) <= tol
+
+
+def test_store_beyond_2_31_scalars_bitwise_at_the_tail(restatement):
+    """3D elasticity f32 with 2^24 + 5 elements: a 2.42 G-scalar store (past
+    the int32 index range; element offsets are 64-bit), ragged last tile and
+    padded last batch.  The first and last 4096 elements and every 65536th
+    in between are bitwise the restatement's."""
+    op, dim, ne = "elasticity", 3, (1 << 24) + 5
+    v, c, _ = fb.mesh_prefix(dim, ne, 0.0, 42)
+    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+    var = fb.make_variant(op, dim, "f32")
+    store = fb.integrate_mesh(var, dv, dc)
+    kr2 = krows(op, dim) ** 2
+    assert store.numel() == var.store_length(ne) and store.numel() > (1 << 31)
+    idx = np.unique(np.concatenate([np.arange(4096), np.arange(0, ne, 65536), np.arange(ne - 4096, ne)]))
+    cs = np.ascontiguousarray(c.reshape(-1, dim + 1)[idx].ravel())
+    want = restatement.integrate_mesh(op, v, cs, dim, bs=1, precision="f32").reshape(-1, kr2)
+    got = store.view(-1, kr2)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert got.tobytes() == want.tobytes()
+    # padding slots (ne .. num_batches*bs) replicate the last element
+    pad = store.view(-1, kr2)[ne:].cpu().numpy()
+    assert pad.shape[0] == var.store_length(ne) // kr2 - ne and pad.shape[0] > 0
+    assert all(p.tobytes() == want[-1].tobytes() for p in pad)
