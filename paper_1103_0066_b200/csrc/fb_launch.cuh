@@ -7,6 +7,10 @@
 #include "fb_devcache.h"
 #include "fb_kernels.cuh"
 
+#ifndef FB_DIRECT32_AUTO
+#define FB_DIRECT32_AUTO 1
+#endif
+
 namespace fbk {
 
 // Library-wide kernel launch counter (exported as fb_launch_counter()).
@@ -77,6 +81,13 @@ cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st
   return cudaGetLastError();
 }
 
+// Shapes whose auto store path is the direct 32-byte per-lane store.
+template <class S, int DIM, int OP>
+constexpr bool direct32_auto()
+{
+  return FB_DIRECT32_AUTO != 0 && sizeof(S) == 4 && DIM == 3 && (OP == kLaplacian || OP == kWeighted);
+}
+
 template <class S, int DIM, int OP, int MODE, bool SYM, bool UNI, bool FROM_G>
 cudaError_t go_store(const LaunchSpec& s, const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st)
 {
@@ -93,8 +104,16 @@ cudaError_t go_store(const LaunchSpec& s, const LaunchArgs& a, const KParamBlob&
     else
       return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStCopy>(a, kb, st);
   default:
-    // auto: the 1D bulk store of linear layouts measured faster than the
-    // LDS/STG copy; the swizzled tensor store measured slower
+    // auto: 3D Laplacian-shaped FP32 matrices (64 B = 2 sectors per element)
+    // leave by per-lane 32-byte stores straight from registers -- no staging
+    // (A/B r02: 3D-L-16M strict 0.79 -> 0.83, fast 0.88 -> 0.93, weighted 3D
+    // 0.84 -> 0.89; FP64, the other shapes and the G-input path lose) -- when
+    // the store is 32-byte aligned; else the 1D
+    // bulk store of linear layouts, measured faster than the LDS/STG copy;
+    // the swizzled tensor store measured slower
+    if constexpr (direct32_auto<S, DIM, OP>() && !FROM_G)  // packed-G input: the copy is faster (0.96 vs 0.94)
+      if ((reinterpret_cast<uintptr_t>(a.out) & 31u) == 0)
+        return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStDirect>(a, kb, st);
     if constexpr (WarpStore<S, DIM, OP, SYM>::TMA == 1)
       return go_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, kStTma>(a, kb, st);
     else
