@@ -328,6 +328,40 @@ def test_unaligned_device_outputs(restatement, prec):
         assert gbuf[1:].cpu().numpy().tobytes() == gwant.tobytes()
 
 
+@pytest.mark.parametrize("op,mode", [("laplacian", "strict"), ("laplacian", "fast"), ("weighted-laplacian", "strict")])
+def test_3d_fp32_direct_stores_and_their_alignment_fallbacks(restatement, op, mode):
+    """3D Laplacian-shaped FP32 stores leave by per-lane 32-byte stores when
+    the output is 32-byte aligned; 16- but not 32-byte aligned outputs take
+    the staged copy, 4-byte aligned ones scalar stores -- every offset gives
+    the same bits (strict: the reference's; fast: the aligned run's)."""
+    import torch
+
+    v, c = mesh(3, 6)
+    ne = c.size // 4
+    w = None
+    if op == "weighted-laplacian":
+        w = np.ascontiguousarray(1.0 + v.reshape(-1, 3)[c.reshape(-1, 4), 0].ravel())
+    var = fb.make_variant(op, 3, "f32", mode, element_batch_size=32)
+    dv, dc = torch.from_numpy(v).cuda(), torch.from_numpy(c).cuda()
+    dw = None if w is None else torch.from_numpy(w).cuda()
+    st = torch.empty(2, dtype=torch.int64, device="cuda")
+    sid = torch.cuda.current_stream().cuda_stream
+    n = var.store_length(ne)
+    buf = torch.empty(n + 8, dtype=torch.float32, device="cuda")
+    assert buf.data_ptr() % 32 == 0
+    got = []
+    for off in (0, 4, 1):  # 32-byte, 16-byte, 4-byte aligned
+        out = buf[off:off + n]
+        out.fill_(float("nan"))
+        fb.status_reset(st, sid)
+        fb.integrate_mesh_async(var, dv, dc, out, st, sid, coefficients=dw)
+        fb.status_check(st, sid)
+        got.append(out.cpu().numpy().tobytes())
+    assert got[0] == got[1] == got[2]
+    if mode == "strict":
+        assert got[0] == restatement.integrate_mesh(op, v, c, 3, bs=32, precision="f32", coeffs=w).tobytes()
+
+
 def test_multi_device_with_device_resident_buffers(restatement):
     """Shards over a device list with device-resident inputs and output: each
     shard stages its slice from / to wherever the buffers live (peer copies
