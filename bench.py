@@ -494,11 +494,24 @@ def main():
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
-        with torch.cuda.graph(graph, stream=cap):
+        try:
+            with torch.cuda.graph(graph, stream=cap):
+                for _ in range(k):
+                    fb.integrate_mesh_async(variant, vtx, cel, output, status, cap.cuda_stream)
+            graph.replay()  # warm
+            torch.cuda.synchronize()
+        except RuntimeError:  # no graph capture here: a launch loop (host-rate bound for tiny kernels)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n0 = fb.launch_counter()
+            torch.cuda._sleep(GAP_CYCLES)
+            e0.record(stream)
             for _ in range(k):
-                fb.integrate_mesh_async(variant, vtx, cel, output, status, cap.cuda_stream)
-        graph.replay()  # warm
-        torch.cuda.synchronize()
+                fb.integrate_mesh_async(variant, vtx, cel, output, status, sid)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            fb.status_check(status, sid)
+            return e0.elapsed_time(e1) / k, fb.launch_counter() - n0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n0 = fb.launch_counter()
         clocks.mark()
