@@ -72,9 +72,9 @@ cudaError_t go_sparse(const LaunchArgs& a, const KParamBlob& kb, cudaStream_t st
   auto kernel = fb_integrate_sparse<S, DIM, OP, MODE, SYM, UNI, FROM_G, ST>;
   constexpr size_t smem = sparse_smem_bytes<S, DIM, OP, SYM, ST>();
   static PerDevice slots;  // one cache per kernel instantiation and device
-  constexpr int threads = kWarpsPerCta * 32;
+  constexpr int threads = sparse_warps<OP>() * 32;
   const int64_t nctas = (a.nloc + threads - 1) / threads;
-  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots, sparse_cta_cap<DIM, OP>(),
+  kernel<<<persistent_grid(kernel, threads, nctas, smem, slots, sparse_cta_cap<DIM, OP>() * 4 / sparse_warps<OP>(),
                            sparse_persistent<S, DIM, OP>()),
            threads, smem, st>>>(a, kp, tm);
   launch_counter().fetch_add(1, std::memory_order_relaxed);

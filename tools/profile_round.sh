@@ -8,6 +8,17 @@
 tag=${1:-r02}
 o=gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $o/${tag}_smi.txt
+# fused-kernel captures first: their DRAM traffic (profiles/ncu_traffic.json,
+# keyed by the kernel-source hash) feeds the bench lines' roofline block
+args=""
+for w in 3d-laplacian-16m 2d-elasticity-1m 3d-elasticity-8m; do
+  for p in f32 f64; do
+    timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_integrate_sparse -s 1 -c 1 \
+        -o $o/${tag}_ncu_${w}_${p} python tools/run_kernel.py --workload $w --precision $p --reps 2 > /dev/null 2>&1
+    args="$args $w:$p:strict $o/${tag}_ncu_${w}_${p}.ncu-rep"
+  done
+done
+python tools/ncu_traffic.py $args > /dev/null && cp profiles/ncu_traffic.json $o/${tag}_ncu_traffic.json
 timeout 900 python bench.py > $o/${tag}_bench_default.json 2> $o/${tag}_bench_default.err
 for w in 2d-elasticity-1m 3d-elasticity-8m 2d-laplacian-64k; do
   timeout 900 python bench.py --workload $w > $o/${tag}_bench_$w.json 2> $o/${tag}_bench_$w.err
@@ -16,12 +27,6 @@ timeout 900 python bench.py --impl reference > $o/${tag}_bench_impl_reference.js
 timeout 300 python tools/hbm_probe.py $o/${tag}_hbm_probe.json > /dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/${tag}_launches_bench_default.csv \
     python bench.py --steps 3 --warmup 3 --e2e-steps 2 --no-cpu-baseline > /dev/null 2>&1
-for w in 3d-laplacian-16m 2d-elasticity-1m 3d-elasticity-8m; do
-  for p in f32 f64; do
-    timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_integrate_sparse -s 1 -c 1 \
-        -o $o/${tag}_ncu_${w}_${p} python tools/run_kernel.py --workload $w --precision $p --reps 2 > /dev/null 2>&1
-  done
-done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_assemble_kernel -s 1 -c 1 \
     -o $o/${tag}_ncu_assemble_3d-laplacian-16m_f32 python tools/asmbench.py --workloads 3d-laplacian-16m --precisions f32 --steps 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:fb_assemble_kernel -s 1 -c 1 \
