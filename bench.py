@@ -485,6 +485,33 @@ def main():
         ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         return statistics.mean(ms), min(ms), launches
 
+    def pcie_floor(h2d_pairs, dout, hout, reps=3):
+        """The copy engines' floor for one e2e step: the step's H2D copies (pinned
+        -> device) and its D2H store copy on two streams at once, plus each
+        direction alone -- raw torch copies, no kernel (best of `reps`)."""
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def run(up, down):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if up:
+                with torch.cuda.stream(s1):
+                    for h, d in h2d_pairs:
+                        d.copy_(h, non_blocking=True)
+            if down:
+                with torch.cuda.stream(s2):
+                    hout.copy_(dout, non_blocking=True)
+            torch.cuda.synchronize()
+            return time.perf_counter() - t0
+
+        both = min(run(True, True) for _ in range(reps))
+        up = min(run(True, False) for _ in range(reps))
+        down = min(run(False, True) for _ in range(reps))
+        nb_up = sum(h.numel() * h.element_size() for h, _ in h2d_pairs)
+        nb_down = hout.numel() * hout.element_size()
+        return {"ms": both * 1e3, "h2d_GBs": nb_up / up * 1e-9, "d2h_GBs": nb_down / down * 1e-9,
+                "what": "the step's H2D and D2H as raw concurrent copies (no kernel); frac = this / e2e ms_per_step"}
+
     def back_to_back(variant, vtx, cel, output, k):
         """k launches captured in one CUDA graph and replayed inside ONE event
         pair, no flush between (device-side steady state: a Python launch loop
@@ -564,6 +591,7 @@ def main():
         e2e_launches = fb.launch_counter() - n0
         barrier()
         e2e_ms = max_over_ranks(e2e_ms)
+        pcie = pcie_floor([(hv, dv), (hc, dc)], out, hout)
         del hout, hout_np
 
         # the other arithmetic mode of the same precision (fast: FP64 edges, then
@@ -692,6 +720,7 @@ def main():
         "e2e": {"value": flops / (e2e_ms * 1e-3) * 1e-9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                 "elements_per_s": ne_per * world / (e2e_ms * 1e-3),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "gpu_launches": e2e_launches,
+                "pcie_floor": dict(pcie, frac=pcie["ms"] / e2e_ms),
                 "api": "fb_integrate_mesh (C ABI), pinned host buffers, chunked H2D/kernel/D2H pipeline"},
         "gpu_launches": launches,
         other: {"value": flops / (ms2 * 1e-3) * 1e-9, "unit": "GFLOP/s", "ms_per_step": ms2,
