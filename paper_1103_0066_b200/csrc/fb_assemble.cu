@@ -96,38 +96,41 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 #ifndef FB_ASM_EVL32
 #define FB_ASM_EVL32 1  // FP32 rows too (A/B: 3D-E f32 1.62 -> 1.59 ms, 3D-L 0.403 -> 0.398)
 #endif
-template <class S, int N, int A>
+// Scalars [T0, N) of the run: at each position the widest load the
+// alignment allows that still fits the tail (a 6-scalar FP32 run on an
+// 8-byte boundary: 3 x 8 B; on 16 B: 16 + 8 B).
+template <class S, int N, int A, int T0 = 0>
 __device__ __forceinline__ void load_vec(const S* p, S (&r)[N])
 {
-  constexpr int W = A / static_cast<int>(sizeof(S)) > 0 ? A / static_cast<int>(sizeof(S)) : 1;  // scalars per load
-  static_assert(N % W == 0, "vector width must divide the run");
-#pragma unroll
-  for (int t = 0; t < N; t += W)
+  if constexpr (T0 < N)
   {
+    constexpr int W0 = A / static_cast<int>(sizeof(S)) > 0 ? A / static_cast<int>(sizeof(S)) : 1;  // scalars per load
+    constexpr int W = T0 + W0 <= N ? W0 : (sizeof(S) == 4 && W0 >= 2 && T0 + 2 <= N ? 2 : 1);
     if constexpr (W == 4)
     {
-      const float4 q = FB_ASM_EVL32 ? ld_el(reinterpret_cast<const float4*>(p + t))
-                                   : __ldg(reinterpret_cast<const float4*>(p + t));
-      r[t] = q.x;
-      r[t + 1] = q.y;
-      r[t + 2] = q.z;
-      r[t + 3] = q.w;
+      const float4 q = FB_ASM_EVL32 ? ld_el(reinterpret_cast<const float4*>(p + T0))
+                                   : __ldg(reinterpret_cast<const float4*>(p + T0));
+      r[T0] = q.x;
+      r[T0 + 1] = q.y;
+      r[T0 + 2] = q.z;
+      r[T0 + 3] = q.w;
     }
     else if constexpr (W == 2 && sizeof(S) == 8)
     {
-      const double2 q = FB_ASM_EVL ? ld_el(reinterpret_cast<const double2*>(p + t))
-                                  : __ldg(reinterpret_cast<const double2*>(p + t));
-      r[t] = q.x;
-      r[t + 1] = q.y;
+      const double2 q = FB_ASM_EVL ? ld_el(reinterpret_cast<const double2*>(p + T0))
+                                  : __ldg(reinterpret_cast<const double2*>(p + T0));
+      r[T0] = q.x;
+      r[T0 + 1] = q.y;
     }
     else if constexpr (W == 2)
     {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(p + t));
-      r[t] = q.x;
-      r[t + 1] = q.y;
+      const float2 q = __ldg(reinterpret_cast<const float2*>(p + T0));
+      r[T0] = q.x;
+      r[T0 + 1] = q.y;
     }
     else
-      r[t] = __ldg(p + t);
+      r[T0] = __ldg(p + T0);
+    load_vec<S, N, A, T0 + W>(p, r);
   }
 }
 
@@ -151,14 +154,27 @@ __host__ __device__ constexpr int gcd_i(int a, int b) { return b == 0 ? a : gcd_
 // Row i = aa + ci*NB of an element matrix, columns j = b + cj*NB for the
 // N = NB*NCW columns of components cj0 .. cj0+NCW-1 (a contiguous run).
 // SYM: A(i, j) == A(j, i), so the run is read from column i, contiguous.
-template <class S, int NB, int KROWS, int N, bool SYM>
+#ifndef FB_ASM_ROWSTART
+#define FB_ASM_ROWSTART 1  // A/B: alignment from the row start alone when cj0 == 0
+#endif
+template <class S, int NB, int KROWS, int N, bool SYM, bool CJ0 = false>
 __device__ __forceinline__ void load_row(const S* blk, int i, int cj0, S (&r)[N])
 {
   if constexpr (SYM)
   {
     // the store is 16-byte aligned (host check); krows^2*s, krows*s and
-    // nb*s are multiples of A, so the run starts on an A-byte boundary
-    constexpr int A = gcd_i(gcd_i(KROWS * static_cast<int>(sizeof(S)), NB * static_cast<int>(sizeof(S))), 16);
+    // nb*s are multiples of A, so the run starts on an A-byte boundary.
+    // CJ0 (the run always starts at column 0: whole rows, or block (0, 0)):
+    // only krows*s matters -- 2D elasticity FP32 rows (24 B) take 8-byte
+    // loads instead of 4-byte ones, FP64 (48 B) 16-byte instead of 8 (A/B
+    // r02, 2D-E-1M: f32 0.102 -> 0.081 ms, f64 0.166 -> 0.134, block
+    // diagonal f64 0.083 -> 0.066; the L1 data pipe was at 84 % with 23
+    // sectors per gather request.  Loading the two aligned 16-byte words that
+    // cover a 24-byte FP32 row and selecting by the misalignment loses:
+    // 0.081 -> 0.102)
+    constexpr int A = (CJ0 && FB_ASM_ROWSTART)
+                          ? gcd_i(KROWS * static_cast<int>(sizeof(S)), 16)
+                          : gcd_i(gcd_i(KROWS * static_cast<int>(sizeof(S)), NB * static_cast<int>(sizeof(S))), 16);
     load_vec<S, N, A>(blk + i * KROWS + cj0 * NB, r);
   }
   else
@@ -292,7 +308,7 @@ __global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS) fb_a
         {
           const int64_t e = pk[u] >> 2;
           const int aa = static_cast<int>(pk[u] & 3u);
-          load_row<S, NB, KROWS, NB * NCW, SYM>(store + e * NK, aa + ci * NB, cj0, r[u]);
+          load_row<S, NB, KROWS, NB * NCW, SYM, (DIAG || NCW == NC)>(store + e * NK, aa + ci * NB, cj0, r[u]);
         }
       // one incidence at a time (two incidences may share a neighbour); with
       // BATCH, the nb*NCW slots of an incidence (distinct: distinct element
