@@ -54,6 +54,14 @@ namespace {
 #ifndef FB_ASM_U2D
 #define FB_ASM_U2D FB_ASM_U
 #endif
+// 2D elasticity, whole rows per warp: 4 incidences in flight (A/B r02,
+// 2D-E-1M: f32 0.082 -> 0.080 ms, f64 0.135 -> 0.121 -- 104 instead of 128
+// registers, 18 resident warps instead of 16; the block-diagonal read keeps
+// 8: f64 0.066 -> 0.080 at 4.  16 in flight loses 1.3-2x; capping the
+// registers for 12 / 16 CTAs spills and loses 2-3x)
+#ifndef FB_ASM_U2E
+#define FB_ASM_U2E 4
+#endif
 // 16 incidences in flight for the latency-bound 3D elasticity FP64 gather and
 // the 3D block-diagonal reads (A/B r02: 3D-E-8M f64 4.65 -> 4.09 ms, block
 // diagonal f64 0.95 -> 0.89, f32 0.59 -> 0.54; 16 everywhere loses up to 2x
@@ -69,7 +77,7 @@ struct AsmShape {
   static constexpr int NCW = (NC == 3 && sizeof(S) == 4) ? 3 : (NC == 2 ? FB_ASM_NCW2 : (NC == 3 ? FB_ASM_NCW3D64 : 1));
   static constexpr int WARPS = NCW == 1 ? 4 : FB_ASM_WARPS_NCW;
   static constexpr int SLOTS = NCW == 1 ? 32 : 24;
-  static constexpr int U = DIM == 2 ? FB_ASM_U2D
+  static constexpr int U = DIM == 2 ? (NC == 2 ? FB_ASM_U2E : FB_ASM_U2D)
                            : (NC == 3 && sizeof(S) == 8 ? FB_ASM_U_3E64 : (NCW == 1 ? FB_ASM_U : 4));
   // prefetch the next chunk's plan entries (registers: 3D elasticity FP64,
   // already at the register limit, is faster without -- A/B measured)
@@ -200,7 +208,11 @@ template <class S, int DIM, int NC, bool DIAG>
 using AsmShapeOf = std::conditional_t<DIAG, AsmShapeDiag<S, DIM>, AsmShape<S, DIM, NC>>;
 
 template <class S, int DIM, int NC, bool SYM, bool DIAG>
-__global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS) fb_assemble_kernel(const AsmArgs a)
+// minBlocks 1 for 2D elasticity: the register allocation it gives the FP64
+// kernel at U = 4 (134 registers) runs 0.121 ms on 2D-E-1M, the
+// unconstrained one (124) 0.209 ms (A/B r02); 0 = unspecified elsewhere
+__global__ void __launch_bounds__(32 * AsmShapeOf<S, DIM, NC, DIAG>::WARPS, DIM == 2 && NC == 2 ? 1 : 0)
+    fb_assemble_kernel(const AsmArgs a)
 {
   using Sh = AsmShapeOf<S, DIM, NC, DIAG>;
   constexpr int NB = DIM + 1, KROWS = NB * NC, NK = KROWS * KROWS;
