@@ -33,6 +33,9 @@ CASES = [  # (path, op, dim, elements)
     ("packed", "laplacian", 3, 1 << 24),
     ("pack_geometry", None, 2, 1 << 20),
     ("pack_geometry", None, 3, 1 << 24),
+    # the 2D launch-size effect: the same kernels at 16M elements
+    ("weighted-fused", "weighted-laplacian", 2, 1 << 24),
+    ("pack_geometry", None, 2, 1 << 24),
 ]
 
 
